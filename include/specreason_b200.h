@@ -1,0 +1,169 @@
+/*
+ * specreason_b200.h -- C-ABI of the B200-native SpecReason inner loop.
+ *
+ * The reference (arXiv 2504.07891, package `stepspec`) has no native code: its
+ * only device crossing is the OpenAI-completions POST of the HTTP backend
+ * (pkg/src/stepspec/backends/http.py:63-94) behind the `Backend` plugin API
+ * (pkg/src/stepspec/backends/base.py:77-100).  This library replaces what sits
+ * behind that POST -- the model server -- with sm_100a kernels; the Python
+ * shim (paper_2504_07891_b200/backend.py) keeps the `Backend` API itself.
+ *
+ * Entry points and the reference interface each one replaces:
+ *
+ *   sr_generate  <- Backend.generate_step (base.py:87-89); semantics of
+ *                   OpenAICompletionsBackend.generate_step (http.py:121-152):
+ *                   prefill the fresh prompt suffix, greedy decode, stop at a
+ *                   stop-class token (kept) or </think> (dropped), else at
+ *                   max_new (finish "length").
+ *   sr_score     <- Backend.score_step (base.py:91-97); semantics of
+ *                   OpenAICompletionsBackend.score_step (http.py:154-174) +
+ *                   extract_score (base.py:106-126) + decide_acceptance
+ *                   (core.py:91-93): one prefill pass, digit readout over the
+ *                   top-10 of the last position, threshold compare.  Only the
+ *                   16-byte sr_readout leaves the GPU.
+ *   page tables  <- _PrefixLedger streams (engine.py:161-186): the caller owns
+ *                   page allocation; truncating a stream (rollback) is just a
+ *                   shorter start_pos on the next call; prefilling the suffix
+ *                   is the commit.
+ *
+ * Ownership: the caller (PyTorch on the Python side) allocates every buffer --
+ * weights, K/V page pools, workspace, outputs.  The library never allocates
+ * device memory for data; it keeps only CUDA graphs and kernel attributes in
+ * the opaque sr_model handle.  All pointers are device pointers unless named
+ * h_*; `stream` is a cudaStream_t passed as void*.
+ *
+ * Errors: every int-returning call returns 0 on success, else a cudaError_t
+ * value or one of SR_E_*; sr_last_error() returns the thread-local message.
+ * Calls on one sr_model must be serialised by the caller (one stream at a
+ * time); distinct models are independent.
+ */
+#ifndef SPECREASON_B200_H
+#define SPECREASON_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SR_ABI_VERSION 1
+#define SR_PAGE 64            /* tokens per K/V page */
+#define SR_HEAD_DIM 128
+
+#define SR_E_INVALID 1001     /* bad descriptor / argument */
+#define SR_E_CAPACITY 1002    /* request exceeds a compiled or declared limit */
+#define SR_E_GRAPH 1003       /* CUDA graph construction failed */
+
+/* finish codes written to sr_generate's output */
+#define SR_FINISH_LENGTH 0
+#define SR_FINISH_STOP 1
+#define SR_FINISH_END_THINK 2
+
+/* token classes of the per-request class table (uint8 per LM-head row) */
+#define SR_CLASS_PLAIN 0
+#define SR_CLASS_STOP 1
+#define SR_CLASS_END_THINK 2
+#define SR_CLASS_MASKED 3
+
+typedef struct sr_model_desc {
+  int32_t n_layers;
+  int32_t d_model;
+  int32_t n_heads;
+  int32_t n_kv_heads;
+  int32_t head_dim;     /* must be SR_HEAD_DIM */
+  int32_t d_ffn;
+  int32_t vocab_rows;   /* embedding / LM-head rows */
+  int32_t vocab_text;   /* rows >= vocab_text are never produced */
+  float rms_eps;
+  int32_t max_pos;      /* rows of the RoPE table; positions must be < max_pos */
+  int32_t max_tokens;   /* largest n_ids of one prefill call */
+  int32_t max_new;      /* largest max_new of one sr_generate call */
+  int32_t n_pages;      /* pages in each of the K and V pools */
+} sr_model_desc;
+
+typedef struct sr_layer_ptrs {
+  const void* ln1;   /* bf16 [d] */
+  const void* wqkv;  /* bf16 [(H + 2*KV)*128, d]: q rows, k rows, v rows */
+  const void* bqkv;  /* bf16 [(H + 2*KV)*128] */
+  const void* wo;    /* bf16 [d, H*128] */
+  const void* ln2;   /* bf16 [d] */
+  const void* wgu;   /* bf16 [2*f, d]: gate/up interleaved in 16-row blocks */
+  const void* wd;    /* bf16 [d, f] */
+} sr_layer_ptrs;
+
+typedef struct sr_model_ptrs {
+  const void* embed;          /* bf16 [vocab_rows, d] */
+  const void* ln_f;           /* bf16 [d] */
+  const void* lm_head;        /* bf16 [vocab_rows, d] */
+  const sr_layer_ptrs* layers;/* host array [n_layers] */
+  const float* rope;          /* fp32 [max_pos, 64, 2] (cos, sin) */
+  void* k_pool;               /* bf16 [n_layers, n_pages, KV, SR_PAGE, 128] */
+  void* v_pool;               /* same */
+  void* workspace;            /* sr_workspace_bytes(desc) bytes, 256-B aligned */
+} sr_model_ptrs;
+
+typedef struct sr_readout {   /* 16 bytes, the only verify output */
+  int32_t score;              /* 0..9, or -1 = no digit (ScoreParseFailure) */
+  int32_t accept;             /* score >= threshold (0 when score == -1) */
+  float margin;               /* best digit logit - runner-up digit logit */
+  int32_t argmax;             /* greedy token at the last position */
+} sr_readout;
+
+typedef struct sr_timing {    /* optional per-call device timings (ms) */
+  float prefill_ms;
+  float decode_ms;
+  int32_t prefill_tokens;
+  int32_t decode_tokens;
+} sr_timing;
+
+int sr_abi_version(void);
+const char* sr_last_error(void);
+
+/* bytes of workspace the caller must provide for `desc` */
+size_t sr_workspace_bytes(const sr_model_desc* desc);
+
+int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* stream,
+                    void** out_model);
+int sr_model_destroy(void* model);
+
+/*
+ * Prefill ids[0..n_ids) at positions start_pos.. of the stream whose page
+ * table is `page_table` (int32, one page id per SR_PAGE positions, covering
+ * start_pos + n_ids + max_new positions), then greedy-decode up to max_new
+ * tokens.  out (int32): out[0] = tokens generated, out[1] = finish code,
+ * out[2 .. 2+max_new) = token ids; margins (fp32 [max_new], may be NULL) =
+ * top-1 minus top-2 logit of each choice.  K/V of every fed token (prompt
+ * suffix and all generated tokens but the last) is resident on return.
+ */
+int sr_generate(void* model, const int32_t* page_table, int32_t start_pos,
+                const int32_t* ids, int32_t n_ids, int32_t max_new,
+                const uint8_t* token_class, int32_t* out, float* margins,
+                void* stream);
+
+/*
+ * Prefill ids at start_pos.. and read the judge digit at the last position:
+ * rank_d = #{v : logit_v > logit_d, or == with v < d}; the best digit with
+ * rank < 10 wins (lower id on ties); else the first digit character of the
+ * greedy token's text (first_digit[v], int8, -1 = none); accept = score >=
+ * threshold.  Writes one sr_readout to `readout` (device).
+ */
+int sr_score(void* model, const int32_t* page_table, int32_t start_pos,
+             const int32_t* ids, int32_t n_ids, const int8_t* first_digit,
+             int32_t threshold, sr_readout* readout, void* stream);
+
+/*
+ * Test hook: prefill ids and write fp32 logits of every new position
+ * (`all` != 0, logits [n_ids, vocab_rows]) or of the last one ([vocab_rows]).
+ */
+int sr_forward_logits(void* model, const int32_t* page_table, int32_t start_pos,
+                      const int32_t* ids, int32_t n_ids, int32_t all, float* logits,
+                      void* stream);
+
+/* device timings of the last sr_generate / sr_score on this model */
+int sr_last_timing(void* model, sr_timing* h_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECREASON_B200_H */

@@ -1,0 +1,290 @@
+"""``B200Backend``: the reference ``Backend`` plugin API on sm_100a kernels.
+
+PyTorch only owns memory here: weights, the K/V page pools, the workspace and
+small staging buffers are torch CUDA tensors whose raw pointers cross the
+C-ABI (``native.py``).  All arithmetic -- prefill, greedy decode with the
+device-side stop test, the judge readout and threshold compare -- runs in the
+native library; per call the host uploads the fresh token ids (4 B each) and
+reads back the generated ids (``sr_generate``) or a 16-byte readout
+(``sr_score``).
+
+Pages: each prefix-cache stream (``host.Stream``) owns a list of page ids and
+a device page table.  Rolling a stream back to its common prefix frees the
+pages past it; a prefill commits new positions into freshly allocated pages.
+When the pool runs dry the least recently used other stream is evicted.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import ctypes as C
+import torch
+
+from . import native
+from .domain import BackendProfile, BackendRole
+from .host import ModelBackend, Readout, Stream
+from .shapes import PAIRS, ModelSpec, get_spec, make_weights, rope_table, tensor_shapes
+from .vocab import Vocab, shared_vocab
+
+PAGE = native.SR_PAGE
+
+
+def first_digit_table(vocab: Vocab, n_rows: int) -> torch.Tensor:
+    """int8 [n_rows]: first '0'-'9' character of each token's text, or -1."""
+    out = torch.full((n_rows,), -1, dtype=torch.int8)
+    for i in range(vocab.n_text):
+        for ch in vocab.render_one(i):
+            if "0" <= ch <= "9":
+                out[i] = ord(ch) - 48
+                break
+    return out
+
+
+class DeviceModel:
+    """One model's weights, K/V page pools, workspace and native handle."""
+
+    def __init__(self, spec: ModelSpec, weights: dict[str, torch.Tensor], *, max_pos: int,
+                 n_pages: int, max_tokens: int = 256, max_new: int = 256,
+                 device: str | torch.device = "cuda") -> None:
+        self.lib = native.load()
+        self.spec = spec
+        self.device = torch.device(device)
+        self.max_pos = max_pos
+        self.max_new = max_new
+        self.n_pages = n_pages
+        self.weights = {k: v.to(self.device, torch.bfloat16).contiguous() for k, v in weights.items()}
+        for name, shape in tensor_shapes(spec).items():
+            if tuple(self.weights[name].shape) != shape:
+                raise ValueError(f"weight {name} has shape {tuple(self.weights[name].shape)}")
+        self.rope = rope_table(spec, max_pos).to(self.device).contiguous()
+        pool_elems = spec.n_layers * n_pages * spec.n_kv_heads * PAGE * spec.head_dim
+        self.k_pool = torch.zeros(pool_elems, dtype=torch.bfloat16, device=self.device)
+        self.v_pool = torch.zeros(pool_elems, dtype=torch.bfloat16, device=self.device)
+        self.desc = native.ModelDesc(
+            n_layers=spec.n_layers, d_model=spec.d_model, n_heads=spec.n_heads,
+            n_kv_heads=spec.n_kv_heads, head_dim=spec.head_dim, d_ffn=spec.d_ffn,
+            vocab_rows=spec.vocab_rows, vocab_text=spec.vocab_text, rms_eps=spec.rms_eps,
+            max_pos=max_pos, max_tokens=max_tokens, max_new=max_new, n_pages=n_pages)
+        ws = self.lib.sr_workspace_bytes(C.byref(self.desc))
+        if ws == 0:
+            raise native.NativeError("sr_workspace_bytes", -1, self.lib.sr_last_error().decode())
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        W = self.weights
+        self._layer_arr = (native.LayerPtrs * spec.n_layers)()
+        for i in range(spec.n_layers):
+            p = f"layers.{i}."
+            self._layer_arr[i] = native.LayerPtrs(*(W[p + n].data_ptr() for n in (
+                "ln1", "wqkv", "bqkv", "wo", "ln2", "wgu", "wd")))
+        ptrs = native.ModelPtrs(
+            embed=W["embed"].data_ptr(), ln_f=W["ln_f"].data_ptr(),
+            lm_head=W["lm_head"].data_ptr(), layers=self._layer_arr,
+            rope=self.rope.data_ptr(), k_pool=self.k_pool.data_ptr(),
+            v_pool=self.v_pool.data_ptr(), workspace=self.workspace.data_ptr())
+        handle = C.c_void_p()
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream().cuda_stream
+            native.check("sr_model_create", self.lib.sr_model_create(
+                C.byref(self.desc), C.byref(ptrs), C.c_void_p(stream), C.byref(handle)))
+        self.handle = handle
+        self.free_pages = list(range(n_pages - 1, -1, -1))
+        # staging
+        self.ids_host = torch.empty(max_pos, dtype=torch.int32, pin_memory=True)
+        self.ids_dev = torch.empty(max_pos, dtype=torch.int32, device=self.device)
+        self.out_dev = torch.zeros(2 + max_new, dtype=torch.int32, device=self.device)
+        self.margin_dev = torch.zeros(max_new, dtype=torch.float32, device=self.device)
+        self.out_host = torch.empty(2 + max_new, dtype=torch.int32, pin_memory=True)
+        self.margin_host = torch.empty(max_new, dtype=torch.float32, pin_memory=True)
+        self.readout_dev = torch.zeros(4, dtype=torch.int32, device=self.device)
+        self.readout_host = torch.empty(4, dtype=torch.int32, pin_memory=True)
+
+    def __del__(self) -> None:
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self.lib.sr_model_destroy(h)
+            except Exception:
+                pass
+
+    @property
+    def stream_ptr(self) -> C.c_void_p:
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def upload_ids(self, ids: Sequence[int]) -> int:
+        n = len(ids)
+        self.ids_host[:n] = torch.as_tensor(ids, dtype=torch.int32)
+        self.ids_dev[:n].copy_(self.ids_host[:n], non_blocking=True)
+        return self.ids_dev.data_ptr()
+
+    def timing(self) -> native.Timing:
+        t = native.Timing()
+        native.check("sr_last_timing", self.lib.sr_last_timing(self.handle, C.byref(t)))
+        return t
+
+
+@dataclass
+class _Pages:
+    pages: list[int]
+    table_dev: torch.Tensor
+    table_host: torch.Tensor
+    synced: int = 0  # entries already uploaded
+
+
+class NativeEngine:
+    """``host.DeviceEngine`` over a ``DeviceModel``."""
+
+    def __init__(self, model: DeviceModel, vocab: Vocab) -> None:
+        self.model = model
+        self.spec = model.spec
+        self.vocab = vocab
+        self.streams: list[Stream] = []
+        self._classes: dict[tuple[str, ...], torch.Tensor] = {}
+        self.first_digit = first_digit_table(vocab, model.spec.vocab_rows).to(model.device)
+        self.max_pages = math.ceil(model.max_pos / PAGE)
+        self.last_margins: list[float] = []
+
+    # -- page management -------------------------------------------------
+    def attach(self, stream: Stream) -> None:
+        stream.handle = _Pages(
+            pages=[],
+            table_dev=torch.zeros(self.max_pages, dtype=torch.int32, device=self.model.device),
+            table_host=torch.zeros(self.max_pages, dtype=torch.int32, pin_memory=True))
+        self.streams.append(stream)
+
+    def truncate(self, stream: Stream, keep: int) -> None:
+        del stream.ids[keep:]
+        pg: _Pages = stream.handle
+        need = math.ceil(keep / PAGE)
+        while len(pg.pages) > need:
+            self.model.free_pages.append(pg.pages.pop())
+        pg.synced = min(pg.synced, len(pg.pages))
+
+    def _ensure(self, stream: Stream, n_positions: int) -> None:
+        if n_positions > self.model.max_pos:
+            raise ValueError(f"context of {n_positions} positions exceeds max_pos "
+                             f"{self.model.max_pos}")
+        pg: _Pages = stream.handle
+        need = math.ceil(n_positions / PAGE)
+        free = self.model.free_pages
+        while len(pg.pages) < need:
+            if not free:
+                victims = sorted((s for s in self.streams if s is not stream and s.handle.pages),
+                                 key=lambda s: s.stamp)
+                if not victims:
+                    raise MemoryError("K/V page pool exhausted")
+                self.truncate(victims[0], 0)
+                continue
+            pg.pages.append(free.pop())
+        if pg.synced < len(pg.pages):
+            lo, hi = pg.synced, len(pg.pages)
+            pg.table_host[lo:hi] = torch.as_tensor(pg.pages[lo:hi], dtype=torch.int32)
+            pg.table_dev[lo:hi].copy_(pg.table_host[lo:hi], non_blocking=True)
+            pg.synced = hi
+
+    def _class_table(self, stop: tuple[str, ...]) -> torch.Tensor:
+        t = self._classes.get(stop)
+        if t is None:
+            cls = self.vocab.token_classes(stop, self.spec.vocab_rows)
+            t = torch.from_numpy(cls.copy()).to(self.model.device)
+            self._classes[stop] = t
+        return t
+
+    # -- engine calls ----------------------------------------------------
+    def generate(self, stream: Stream, suffix: Sequence[int], max_new: int,
+                 stop: tuple[str, ...]) -> tuple[list[int], int]:
+        m = self.model
+        max_new = min(max_new, m.max_new)
+        start = len(stream.ids)
+        self._ensure(stream, start + len(suffix) + max_new)
+        cls = self._class_table(stop)
+        ids_ptr = m.upload_ids(suffix)
+        native.check("sr_generate", m.lib.sr_generate(
+            m.handle, C.c_void_p(stream.handle.table_dev.data_ptr()), start,
+            C.c_void_p(ids_ptr), len(suffix), max_new, C.c_void_p(cls.data_ptr()),
+            C.c_void_p(m.out_dev.data_ptr()), C.c_void_p(m.margin_dev.data_ptr()),
+            m.stream_ptr))
+        m.out_host.copy_(m.out_dev, non_blocking=True)
+        m.margin_host.copy_(m.margin_dev, non_blocking=True)
+        torch.cuda.current_stream(m.device).synchronize()
+        n, finish = int(m.out_host[0]), int(m.out_host[1])
+        gen = m.out_host[2:2 + n].tolist()
+        self.last_margins = m.margin_host[:n].tolist()
+        stream.ids.extend(suffix)
+        stream.ids.extend(gen[:-1])
+        return gen, finish
+
+    def score(self, stream: Stream, suffix: Sequence[int], threshold: int) -> Readout:
+        m = self.model
+        start = len(stream.ids)
+        self._ensure(stream, start + len(suffix))
+        ids_ptr = m.upload_ids(suffix)
+        native.check("sr_score", m.lib.sr_score(
+            m.handle, C.c_void_p(stream.handle.table_dev.data_ptr()), start,
+            C.c_void_p(ids_ptr), len(suffix), C.c_void_p(self.first_digit.data_ptr()),
+            int(threshold), C.c_void_p(m.readout_dev.data_ptr()), m.stream_ptr))
+        m.readout_host.copy_(m.readout_dev, non_blocking=True)
+        torch.cuda.current_stream(m.device).synchronize()
+        stream.ids.extend(suffix)
+        r = m.readout_host
+        margin = r[2:3].view(torch.float32).item()
+        return Readout(score=int(r[0]), accept=bool(int(r[1])), flags=0, margin=margin,
+                       argmax=int(r[3]))
+
+    def forward_logits(self, stream: Stream, suffix: Sequence[int], all_rows: bool = True) -> torch.Tensor:
+        """Test hook: prefill ``suffix`` and return fp32 logits (device)."""
+        m = self.model
+        start = len(stream.ids)
+        self._ensure(stream, start + len(suffix))
+        ids_ptr = m.upload_ids(suffix)
+        rows = len(suffix) if all_rows else 1
+        out = torch.empty(rows, self.spec.vocab_rows, dtype=torch.float32, device=m.device)
+        native.check("sr_forward_logits", m.lib.sr_forward_logits(
+            m.handle, C.c_void_p(stream.handle.table_dev.data_ptr()), start,
+            C.c_void_p(ids_ptr), len(suffix), 1 if all_rows else 0,
+            C.c_void_p(out.data_ptr()), m.stream_ptr))
+        torch.cuda.current_stream(m.device).synchronize()
+        stream.ids.extend(suffix)
+        return out
+
+
+class B200Backend(ModelBackend):
+    """Drop-in ``Backend`` whose model runs on the B200 (see module doc)."""
+
+    def __init__(self, spec: ModelSpec | str, role: BackendRole, *, seed: int = 0,
+                 weights: dict[str, torch.Tensor] | None = None, max_ctx: int = 8192,
+                 n_streams: int = 4, threshold: int = 7, max_new: int = 256,
+                 max_tokens: int = 256, device: str = "cuda", init_device: str | None = None,
+                 vocab: Vocab | None = None, types=None, record: bool = False) -> None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("B200Backend needs a CUDA device (no CPU fallback)")
+        spec = get_spec(spec) if isinstance(spec, str) else spec
+        if weights is None:
+            init_device = init_device or ("cpu" if spec.d_model <= 512 else device)
+            weights = make_weights(spec, seed, device=init_device)
+        max_pos = max_ctx + max_new + 64
+        pages_per_stream = math.ceil(max_pos / PAGE) + 1
+        model = DeviceModel(spec, weights, max_pos=max_pos, n_pages=n_streams * pages_per_stream,
+                            max_tokens=max_tokens, max_new=max_new, device=device)
+        vocab = vocab or shared_vocab(spec.vocab_text)
+        T = types
+        prof_cls = T.BackendProfile if T else BackendProfile
+        role_cls = T.BackendRole if T else BackendRole
+        profile = prof_cls(name=f"b200-{spec.name}", role=role_cls(role.value),
+                           decode_s_per_token=spec.decode_bytes(0) / 6.4e12,
+                           prefill_tokens_per_s=1e4)
+        self.device_model = model
+        super().__init__(NativeEngine(model, vocab), vocab, profile, n_streams=n_streams,
+                         threshold=threshold, types=types, record=record)
+
+
+def build_pair(pair: str = "tiny", *, seed: int = 0, max_ctx: int = 8192, threshold: int = 7,
+               types=None, record: bool = False, **kw) -> tuple[B200Backend, B200Backend]:
+    """(small, base) backends for a named model pair (``shapes.PAIRS``)."""
+    small_name, base_name = PAIRS[pair]
+    small = B200Backend(small_name, BackendRole.SMALL, seed=seed, max_ctx=max_ctx,
+                        threshold=threshold, types=types, record=record, **kw)
+    base = B200Backend(base_name, BackendRole.BASE, seed=seed, max_ctx=max_ctx,
+                       threshold=threshold, types=types, record=record, **kw)
+    return small, base

@@ -1,0 +1,152 @@
+// Kernel parameter blocks and host launchers shared by the runtime.
+#pragma once
+
+#include "common.cuh"
+
+namespace sr {
+
+// ------------------------------------------------------------------ GEMV ---
+enum GemvKind {
+  GEMV_QKV_EMBED,   // embed gather + RMSNorm -> qkv + bias + RoPE + K/V append
+  GEMV_QKV,         // RMSNorm(h) -> qkv + bias + RoPE + K/V append
+  GEMV_RESID,       // x -> h += W x
+  GEMV_GLU,         // RMSNorm(h) -> silu(gate) * up
+  GEMV_LM_ARGMAX,   // RMSNorm(h) -> logits -> greedy token (+ stop test)
+  GEMV_LM_ARGMAX_X, // normalised x -> logits -> greedy token
+  GEMV_LM_LOGITS_X, // normalised x -> fp32 logits
+};
+
+struct GemvParams {
+  const __nv_bfloat16* W;
+  int N, K, n_tasks, n_valid;
+  const __nv_bfloat16* x;
+  float* h;
+  const __nv_bfloat16* embed;
+  const __nv_bfloat16* norm_w;
+  float eps;
+  // qkv epilogue
+  const __nv_bfloat16* bias;
+  const float* rope;
+  __nv_bfloat16* qout;
+  __nv_bfloat16* k_pool;
+  __nv_bfloat16* v_pool;
+  int layer, n_pages, n_kv, q_dim, kv_dim;
+  // glu / logits epilogues
+  __nv_bfloat16* act_out;
+  float* logits;
+  // argmax epilogue
+  float* part_v1;
+  float* part_v2;
+  int* part_i1;
+  unsigned int* counter;
+  DecodeState* st;
+};
+
+cudaError_t gemv_launch(GemvKind kind, GemvParams p, int num_sms, cudaStream_t stream, bool pdl);
+int gemv_max_grid(int num_sms);
+
+// Greedy choice bookkeeping + stop test, run by one thread (host mirror:
+// paper_2504_07891_b200.host.finish_of).
+SR_DEV void select_token(DecodeState* st, int t, float margin) {
+  const int n = st->n_gen;
+  st->out_ids[n] = t;
+  if (st->margins) st->margins[n] = margin;
+  const int cls = st->token_class[t];
+  int done = 0, finish = SR_FINISH_LENGTH;
+  if (cls == SR_CLASS_END_THINK) {
+    done = 1;
+    finish = SR_FINISH_END_THINK;
+  } else if (cls == SR_CLASS_STOP) {
+    done = 1;
+    finish = SR_FINISH_STOP;
+  } else if (n + 1 >= st->max_new) {
+    done = 1;
+  }
+  st->n_gen = n + 1;
+  st->done = done;
+  st->finish = finish;
+  if (!done) {
+    st->token = t;
+    st->pos = st->pos + 1;
+    st->ctx_len = st->pos + 1;
+  }
+  st->out_hdr[0] = n + 1;
+  st->out_hdr[1] = finish;
+  if (st->cond_handle)
+    cudaGraphSetConditional((cudaGraphConditionalHandle)st->cond_handle, done ? 0u : 1u);
+}
+
+// ------------------------------------------------------------- attention ---
+struct AttnParams {
+  const __nv_bfloat16* q;    // [M, H*128] (decode: M = 1)
+  __nv_bfloat16* out;        // [M, H*128]
+  const __nv_bfloat16* k_pool;
+  const __nv_bfloat16* v_pool;
+  const int* page_table;     // prefill; decode reads st->page_table
+  float* part;               // [M, H, nsplit, 128 + 2]
+  unsigned int* counters;    // [M, KV]
+  int layer, n_pages, n_heads, n_kv, nsplit;
+  int start_pos;             // prefill: position of row 0
+  DecodeState* st;           // decode: ctx_len / page table from here
+};
+
+cudaError_t attn_decode_launch(const AttnParams& p, cudaStream_t stream, bool pdl);
+cudaError_t attn_prefill_launch(const AttnParams& p, int M, cudaStream_t stream);
+
+// ----------------------------------------------------------- prefill path ---
+// C_partial[s][m][n] = sum_{k in split s} A[m][k] * B[n][k]
+struct GemmParams {
+  const __nv_bfloat16* A;  // [M, K]
+  const __nv_bfloat16* B;  // [N, K]
+  float* C;                // [splits, M, N]
+  int M, N, K, splits;
+};
+cudaError_t gemm_launch(const GemmParams& p, cudaStream_t stream);
+int gemm_pick_splits(int M, int N, int K, int num_sms);
+
+struct EpiParams {
+  const float* part;   // [splits, M, N]
+  int splits, M, N;
+  // residual + norm
+  float* h;            // [M, d]
+  const __nv_bfloat16* norm_w;
+  float eps;
+  __nv_bfloat16* x;    // [M, d] normalised output
+  // qkv
+  const __nv_bfloat16* bias;
+  const float* rope;
+  __nv_bfloat16* q;    // [M, q_dim]
+  __nv_bfloat16* k_pool;
+  __nv_bfloat16* v_pool;
+  const int* page_table;
+  int start_pos, layer, n_pages, n_kv, q_dim, kv_dim;
+  // glu
+  __nv_bfloat16* act;  // [M, f]
+};
+
+cudaError_t embed_norm_launch(const int* ids, int M, const __nv_bfloat16* embed, int d,
+                              const __nv_bfloat16* norm_w, float eps, float* h,
+                              __nv_bfloat16* x, cudaStream_t stream);
+cudaError_t epi_qkv_launch(const EpiParams& p, cudaStream_t stream);
+cudaError_t epi_resid_norm_launch(const EpiParams& p, cudaStream_t stream);
+cudaError_t epi_glu_launch(const EpiParams& p, cudaStream_t stream);
+
+// verify readout over fp32 logits [V]
+struct ReadoutParams {
+  const float* logits;
+  int n_valid;
+  const int8_t* first_digit;
+  int threshold;
+  unsigned int* counts;  // [10] + [1] block counter
+  float* part_v1;
+  float* part_v2;
+  int* part_i1;
+  sr_readout* out;
+};
+cudaError_t readout_launch(const ReadoutParams& p, int num_sms, cudaStream_t stream);
+
+// decode-loop bookkeeping kernels
+cudaError_t decode_begin_launch(DecodeState* st, const DecodeState* h_init, cudaStream_t stream);
+cudaError_t cond_init_launch(DecodeState* st, unsigned long long handle, cudaStream_t stream);
+
+}  // namespace sr

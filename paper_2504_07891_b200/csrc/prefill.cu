@@ -1,0 +1,373 @@
+// Prefill path (prompt suffixes and verification passes, M >= 1 tokens):
+// embedding + RMSNorm, split-K GEMM partials, and the reduce-epilogues that
+// finish each projection (bias + RoPE + K/V page append; residual add fused
+// with the next RMSNorm; SiLU * up), plus the verify readout (K8).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sr {
+
+// ============================================================== GEMM (v1) ==
+// C[s][m][n] = sum_k A[m][k] * B[n][k] over split s's K range.
+// Tile 64 (tokens) x 128 (weight rows) x 32, 8 warps (2 x 4), warp tile 32x32,
+// mma.sync m16n8k16 bf16 -> fp32, 3-stage cp.async ring, ldmatrix fragments.
+constexpr int BM = 64, BN = 128, BK = 32, STAGES = 3;
+constexpr int LDS = BK + 8;  // padded row (80 B): conflict-free ldmatrix
+
+SR_DEV void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n));
+}
+SR_DEV void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+SR_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+SR_DEV void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(s));
+}
+
+SR_DEV void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(256) gemm_mma_kernel(GemmParams p) {
+  __shared__ __align__(16) __nv_bfloat16 As[STAGES][BM][LDS];
+  __shared__ __align__(16) __nv_bfloat16 Bs[STAGES][BN][LDS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, split = blockIdx.z;
+  const int k_per = ((p.K / BK + p.splits - 1) / p.splits) * BK;
+  const int kbeg = split * k_per;
+  const int kend = min(p.K, kbeg + k_per);
+  const int nk = kend > kbeg ? (kend - kbeg) / BK : 0;
+
+  auto load_stage = [&](int st, int kt) {
+    const int k0 = kbeg + kt * BK;
+    // A: 64 rows x 32 cols = 256 x 16B chunks (one per thread)
+    {
+      const int r = tid >> 2, c = (tid & 3) * 8;
+      const int gm = m0 + r;
+      const bool ok = gm < p.M;
+      cp_async16(&As[st][r][c], p.A + (size_t)(ok ? gm : 0) * p.K + k0 + c, ok);
+    }
+    // B: 128 rows x 32 cols = 512 chunks (two per thread)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int idx = tid + i * 256;
+      const int r = idx >> 2, c = (idx & 3) * 8;
+      const int gn = n0 + r;
+      const bool ok = gn < p.N;
+      cp_async16(&Bs[st][r][c], p.B + (size_t)(ok ? gn : 0) * p.K + k0 + c, ok);
+    }
+  };
+
+  float acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.f;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + STAGES - 1;
+    if (nxt < nk) load_stage(nxt % STAGES, nxt);
+    cp_commit();
+    const int st = kt % STAGES;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 16) {
+      uint32_t a[2][4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = wm * 32 + i * 16 + (lane & 15);
+        const int c = kk + (lane >> 4) * 8;
+        ldsm_x4(a[i][0], a[i][1], a[i][2], a[i][3], &As[st][r][c]);
+      }
+      uint32_t b[4][2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {  // two x4 loads = four n8 tiles
+        const int r = wn * 32 + j * 16 + (lane >> 4) * 8 + (lane & 7);
+        const int c = kk + ((lane >> 3) & 1) * 8;
+        uint32_t r0, r1, r2, r3;
+        ldsm_x4(r0, r1, r2, r3, &Bs[st][r][c]);
+        b[2 * j][0] = r0; b[2 * j][1] = r1; b[2 * j + 1][0] = r2; b[2 * j + 1][1] = r3;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mma16816(acc[i][j], a[i], b[j][0], b[j][1]);
+    }
+  }
+  cp_wait<0>();
+
+  float* C = p.C + (size_t)split * p.M * p.N;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = n0 + wn * 32 + j * 8 + 2 * t;
+#pragma unroll
+      for (int hrow = 0; hrow < 2; ++hrow) {
+        const int row = m0 + wm * 32 + i * 16 + g + hrow * 8;
+        if (row < p.M && col < p.N) {
+          float2 v = make_float2(acc[i][j][2 * hrow], acc[i][j][2 * hrow + 1]);
+          if (col + 1 < p.N) *reinterpret_cast<float2*>(C + (size_t)row * p.N + col) = v;
+          else C[(size_t)row * p.N + col] = v.x;
+        }
+      }
+    }
+}
+
+int gemm_pick_splits(int M, int N, int K, int num_sms) {
+  const int tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+  int s = 1;
+  while (tiles * s < num_sms && (K / BK) / (s * 2) >= 8 && s < 16) s *= 2;
+  return s;
+}
+
+cudaError_t gemm_launch(const GemmParams& p, cudaStream_t stream) {
+  if (p.K % BK != 0) return cudaErrorInvalidValue;
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.splits);
+  gemm_mma_kernel<<<grid, 256, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// ========================================================= epilogues ======
+constexpr int kEpiThreads = 256;
+
+// h[m] = embed[ids[m]];  x[m] = bf16(rmsnorm(h[m]) * w)
+__global__ void embed_norm_kernel(const int* ids, const __nv_bfloat16* embed, int d,
+                                  const __nv_bfloat16* w, float eps, float* h, __nv_bfloat16* x) {
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  const __nv_bfloat16* e = embed + (size_t)ids[m] * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = bf_to_f(e[i]);
+    h[(size_t)m * d + i] = v;
+    ss += v * v;
+  }
+  ss = block_sum(ss, red);
+  const float rstd = rsqrtf(ss / d + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+    x[(size_t)m * d + i] = __float2bfloat16_rn(bf_to_f(e[i]) * rstd * bf_to_f(w[i]));
+}
+
+cudaError_t embed_norm_launch(const int* ids, int M, const __nv_bfloat16* embed, int d,
+                              const __nv_bfloat16* norm_w, float eps, float* h,
+                              __nv_bfloat16* x, cudaStream_t stream) {
+  embed_norm_kernel<<<M, kEpiThreads, 0, stream>>>(ids, embed, d, norm_w, eps, h, x);
+  return cudaGetLastError();
+}
+
+SR_DEV float sum_splits(const float* part, int splits, size_t stride, size_t idx) {
+  float v = 0.f;
+  for (int s = 0; s < splits; ++s) v += part[s * stride + idx];
+  return v;
+}
+
+// q/k: bias + RoPE (pairs j, j+64); k, v -> pages; q -> bf16 buffer
+__global__ void epi_qkv_kernel(EpiParams p) {
+  const int m = blockIdx.x;
+  const int pos = p.start_pos + m;
+  const size_t stride = (size_t)p.M * p.N;
+  const int qk = p.q_dim + p.kv_dim;
+  const int n_pairs = p.N / 2;
+  const int page = p.page_table[pos / kPage];
+  for (int t = threadIdx.x; t < n_pairs; t += blockDim.x) {
+    int r0, r1;
+    if (t < qk / 2) { r0 = (t / kHalf) * kHeadDim + t % kHalf; r1 = r0 + kHalf; }
+    else { r0 = qk + 2 * (t - qk / 2); r1 = r0 + 1; }
+    const float v0 = sum_splits(p.part, p.splits, stride, (size_t)m * p.N + r0) + bf_to_f(p.bias[r0]);
+    const float v1 = sum_splits(p.part, p.splits, stride, (size_t)m * p.N + r1) + bf_to_f(p.bias[r1]);
+    if (r0 < qk) {
+      const int j = r0 % kHeadDim;
+      const float c = p.rope[((size_t)pos * kHalf + j) * 2];
+      const float s = p.rope[((size_t)pos * kHalf + j) * 2 + 1];
+      const float y0 = v0 * c - v1 * s, y1 = v1 * c + v0 * s;
+      if (r0 < p.q_dim) {
+        p.q[(size_t)m * p.q_dim + r0] = __float2bfloat16_rn(y0);
+        p.q[(size_t)m * p.q_dim + r1] = __float2bfloat16_rn(y1);
+      } else {
+        const int kvh = (r0 - p.q_dim) / kHeadDim;
+        const size_t base = kv_offset(p.layer, page, kvh, pos % kPage, p.n_pages, p.n_kv);
+        p.k_pool[base + j] = __float2bfloat16_rn(y0);
+        p.k_pool[base + j + kHalf] = __float2bfloat16_rn(y1);
+      }
+    } else {
+      const int vr = r0 - qk, kvh = vr / kHeadDim, dd = vr % kHeadDim;
+      const size_t base = kv_offset(p.layer, page, kvh, pos % kPage, p.n_pages, p.n_kv);
+      p.v_pool[base + dd] = __float2bfloat16_rn(v0);
+      p.v_pool[base + dd + 1] = __float2bfloat16_rn(v1);
+    }
+  }
+}
+
+cudaError_t epi_qkv_launch(const EpiParams& p, cudaStream_t stream) {
+  epi_qkv_kernel<<<p.M, kEpiThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// h[m] += sum_s part;  x[m] = bf16(rmsnorm(h[m]) * w)   (N == d)
+__global__ void epi_resid_norm_kernel(EpiParams p) {
+  extern __shared__ float hrow[];
+  __shared__ float red[32];
+  const int m = blockIdx.x, d = p.N;
+  const size_t stride = (size_t)p.M * p.N;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = p.h[(size_t)m * d + i] + sum_splits(p.part, p.splits, stride, (size_t)m * d + i);
+    p.h[(size_t)m * d + i] = v;
+    hrow[i] = v;
+    ss += v * v;
+  }
+  ss = block_sum(ss, red);
+  const float rstd = rsqrtf(ss / d + p.eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+    p.x[(size_t)m * d + i] = __float2bfloat16_rn(hrow[i] * rstd * bf_to_f(p.norm_w[i]));
+}
+
+cudaError_t epi_resid_norm_launch(const EpiParams& p, cudaStream_t stream) {
+  epi_resid_norm_kernel<<<p.M, kEpiThreads, p.N * sizeof(float), stream>>>(p);
+  return cudaGetLastError();
+}
+
+// act[m][u] = bf16(silu(gate) * up) from interleaved 16-row blocks
+__global__ void epi_glu_kernel(EpiParams p) {
+  const int m = blockIdx.y;
+  const int f = p.N / 2;
+  const size_t stride = (size_t)p.M * p.N;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < f; u += gridDim.x * blockDim.x) {
+    const int b = u >> 4, j = u & 15;
+    const float g = sum_splits(p.part, p.splits, stride, (size_t)m * p.N + 32 * b + j);
+    const float v = sum_splits(p.part, p.splits, stride, (size_t)m * p.N + 32 * b + 16 + j);
+    p.act[(size_t)m * f + u] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * v);
+  }
+}
+
+cudaError_t epi_glu_launch(const EpiParams& p, cudaStream_t stream) {
+  const int f = p.N / 2;
+  dim3 grid((f + kEpiThreads - 1) / kEpiThreads, p.M);
+  epi_glu_kernel<<<grid, kEpiThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// ======================================================= verify readout ====
+// Pass 1 (grid-wide): greedy top-2 partials and, for each digit d, the count
+// of valid ids ranked before it (logit greater, or equal with a lower id).
+// The last CTA applies extract_score's preference order and the threshold.
+constexpr int kReadoutThreads = 256;
+
+__global__ void __launch_bounds__(kReadoutThreads) readout_kernel(ReadoutParams p) {
+  __shared__ float dig[10];
+  __shared__ unsigned int cnt[10];
+  __shared__ float s_v1[8], s_v2[8];
+  __shared__ int s_i1[8];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 10) { dig[tid] = p.logits[tid]; cnt[tid] = 0; }
+  __syncthreads();
+  float dl[10];
+#pragma unroll
+  for (int d = 0; d < 10; ++d) dl[d] = dig[d];
+  unsigned int c[10];
+#pragma unroll
+  for (int d = 0; d < 10; ++d) c[d] = 0;
+  Top2 best;
+  best.init();
+  for (int v = blockIdx.x * blockDim.x + tid; v < p.n_valid; v += gridDim.x * blockDim.x) {
+    const float x = p.logits[v];
+    best.push(x, v);
+#pragma unroll
+    for (int d = 0; d < 10; ++d) c[d] += (x > dl[d] || (x == dl[d] && v < d)) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int d = 0; d < 10; ++d) {
+    unsigned int s = c[d];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) atomicAdd(&cnt[d], s);
+  }
+  warp_top2(best);
+  if (lane == 0) { s_v1[warp] = best.v1; s_v2[warp] = best.v2; s_i1[warp] = best.i1; }
+  __syncthreads();
+  if (tid == 0) {
+    Top2 b;
+    b.init();
+    for (int w = 0; w < kReadoutThreads / 32; ++w) b.merge(s_v1[w], s_i1[w], s_v2[w]);
+    p.part_v1[blockIdx.x] = b.v1;
+    p.part_v2[blockIdx.x] = b.v2;
+    p.part_i1[blockIdx.x] = b.i1;
+    for (int d = 0; d < 10; ++d) atomicAdd(&p.counts[d], cnt[d]);
+    __threadfence();
+    const unsigned prev = atomicAdd(&p.counts[10], 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last || tid != 0) return;
+  __threadfence();
+  Top2 g;
+  g.init();
+  for (int i = 0; i < (int)gridDim.x; ++i)
+    g.merge(__ldcg(p.part_v1 + i), __ldcg(p.part_i1 + i), __ldcg(p.part_v2 + i));
+  int best_d = -1;
+  float best_v = -INFINITY, second = -INFINITY;
+  for (int d = 0; d < 10; ++d) {
+    const unsigned rank = __ldcg(&p.counts[d]);
+    if (rank >= 10 || d >= p.n_valid) continue;
+    const float v = dig[d];
+    if (best_d < 0 || v > best_v) { second = best_v; best_v = v; best_d = d; }
+    else if (v > second) second = v;
+  }
+  int score = best_d;
+  if (score < 0) score = p.first_digit[g.i1];
+  sr_readout r;
+  r.score = score;
+  r.accept = (score >= 0 && score >= p.threshold) ? 1 : 0;
+  r.margin = best_d >= 0 ? best_v - second : 0.f;
+  r.argmax = g.i1;
+  *p.out = r;
+  for (int d = 0; d <= 10; ++d) p.counts[d] = 0;
+}
+
+cudaError_t readout_launch(const ReadoutParams& p, int num_sms, cudaStream_t stream) {
+  readout_kernel<<<num_sms, kReadoutThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// ===================================================== decode bookkeeping ===
+__global__ void decode_begin_kernel(DecodeState* st, DecodeState init) { *st = init; }
+
+cudaError_t decode_begin_launch(DecodeState* st, const DecodeState* h_init, cudaStream_t stream) {
+  decode_begin_kernel<<<1, 1, 0, stream>>>(st, *h_init);
+  return cudaGetLastError();
+}
+
+// First node of the decode graph: arm the while-loop from the prefill's choice.
+__global__ void cond_init_kernel(DecodeState* st, unsigned long long handle) {
+  st->cond_handle = handle;
+  cudaGraphSetConditional((cudaGraphConditionalHandle)handle, st->done ? 0u : 1u);
+}
+
+cudaError_t cond_init_launch(DecodeState* st, unsigned long long handle, cudaStream_t stream) {
+  cond_init_kernel<<<1, 1, 0, stream>>>(st, handle);
+  return cudaGetLastError();
+}
+
+}  // namespace sr

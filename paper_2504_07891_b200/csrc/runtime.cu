@@ -1,0 +1,575 @@
+// Native runtime behind the C-ABI (include/specreason_b200.h).
+//
+// A model handle carves the caller's workspace into activation buffers and a
+// DecodeState, and owns one CUDA graph per model:
+//
+//   [cond_init] -> WHILE(cond) { layer 0..L-1: qkv GEMV | attention | o GEMV |
+//                                gate/up GEMV | down GEMV ;  LM-head argmax }
+//
+// The LM-head kernel's last CTA chooses the token, runs the stop test and sets
+// the while-condition from the device (cudaGraphSetConditional), so a whole
+// step's decode is one graph launch with no host round trip per token (K10).
+// Kernels inside the body are chained with programmatic dependent launch, so
+// each GEMV's weight prefetch overlaps its predecessor's tail.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sr {
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define SR_CK(expr)                                                                      \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail((int)_e, std::string(#expr) + ": " + cudaGetErrorString(_e));         \
+  } while (0)
+
+constexpr int kPrefillSplitsMax = 4;
+constexpr int kAttnPrefillSplit = 8;
+
+struct Layout {  // workspace carve-up (byte offsets)
+  size_t st, h, x, q, attn, act, part, apart, actr, lm_v1, lm_v2, lm_i1, lm_ctr, logits, ro_cnt,
+      total;
+  int nsplit_decode;
+  size_t part_floats;
+};
+
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+static Layout make_layout(const sr_model_desc& d, int num_sms) {
+  Layout L{};
+  const size_t T = d.max_tokens;
+  const size_t qd = (size_t)d.n_heads * SR_HEAD_DIM;
+  const size_t qkv = qd + 2 * (size_t)d.n_kv_heads * SR_HEAD_DIM;
+  const size_t nmax = std::max<size_t>({qkv, (size_t)d.d_model, 2 * (size_t)d.d_ffn});
+  L.nsplit_decode = std::max(1, (2 * num_sms + d.n_kv_heads - 1) / d.n_kv_heads);
+  const size_t nsplit_max = std::max<size_t>(L.nsplit_decode, kAttnPrefillSplit);
+  const size_t lm_parts = (size_t)gemv_max_grid(num_sms) + 64;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+  L.st = take(sizeof(DecodeState));
+  L.h = take(T * d.d_model * 4);
+  L.x = take(T * std::max<size_t>(d.d_model, qd) * 2);
+  L.q = take(T * qd * 2);
+  L.attn = take(T * qd * 2);
+  L.act = take(T * d.d_ffn * 2);
+  L.part_floats = (size_t)kPrefillSplitsMax * T * nmax;
+  L.part = take(L.part_floats * 4);
+  L.apart = take(T * d.n_heads * nsplit_max * (SR_HEAD_DIM + 2) * 4);
+  L.actr = take(T * d.n_kv_heads * 4);
+  L.lm_v1 = take(lm_parts * 4);
+  L.lm_v2 = take(lm_parts * 4);
+  L.lm_i1 = take(lm_parts * 4);
+  L.lm_ctr = take(64);
+  L.logits = take((size_t)d.vocab_rows * 4);
+  L.ro_cnt = take(64);
+  L.total = o;
+  return L;
+}
+
+struct Model {
+  sr_model_desc d;
+  std::vector<sr_layer_ptrs> layers;
+  const __nv_bfloat16 *embed, *ln_f, *lm_head;
+  const float* rope;
+  __nv_bfloat16 *k_pool, *v_pool;
+  Layout L;
+  char* ws;
+  int num_sms;
+  int q_dim, kv_dim, qkv_rows;
+  DecodeState* st;
+  float* h;
+  __nv_bfloat16 *x, *q, *attn, *act;
+  float *part, *apart, *lm_v1, *lm_v2, *logits;
+  int* lm_i1;
+  unsigned *actr, *lm_ctr, *ro_cnt;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphConditionalHandle cond = 0;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  sr_timing timing{};
+  bool pdl = true;
+
+  template <typename T>
+  T* at(size_t off) { return reinterpret_cast<T*>(ws + off); }
+
+  const __nv_bfloat16* lw(int l, int which) const {
+    const sr_layer_ptrs& p = layers[l];
+    const void* v[] = {p.ln1, p.wqkv, p.bqkv, p.wo, p.ln2, p.wgu, p.wd};
+    return reinterpret_cast<const __nv_bfloat16*>(v[which]);
+  }
+  enum { LN1, WQKV, BQKV, WO, LN2, WGU, WD };
+
+  GemvParams gemv_base() const {
+    GemvParams p{};
+    p.eps = d.rms_eps;
+    p.rope = rope;
+    p.k_pool = k_pool;
+    p.v_pool = v_pool;
+    p.n_pages = d.n_pages;
+    p.n_kv = d.n_kv_heads;
+    p.q_dim = q_dim;
+    p.kv_dim = kv_dim;
+    p.h = h;
+    p.st = st;
+    return p;
+  }
+
+  // ------------------------------------------------------- decode step ----
+  cudaError_t enqueue_decode_step(cudaStream_t s) {
+    cudaError_t e;
+    for (int l = 0; l < d.n_layers; ++l) {
+      GemvParams p = gemv_base();
+      p.layer = l;
+      p.W = lw(l, WQKV);
+      p.N = qkv_rows;
+      p.K = d.d_model;
+      p.norm_w = lw(l, LN1);
+      p.bias = lw(l, BQKV);
+      p.embed = embed;
+      p.qout = q;
+      e = gemv_launch(l == 0 ? GEMV_QKV_EMBED : GEMV_QKV, p, num_sms, s, pdl && l > 0);
+      if (e != cudaSuccess) return e;
+
+      AttnParams a{};
+      a.q = q;
+      a.out = attn;
+      a.k_pool = k_pool;
+      a.v_pool = v_pool;
+      a.part = apart;
+      a.counters = actr;
+      a.layer = l;
+      a.n_pages = d.n_pages;
+      a.n_heads = d.n_heads;
+      a.n_kv = d.n_kv_heads;
+      a.nsplit = L.nsplit_decode;
+      a.st = st;
+      e = attn_decode_launch(a, s, pdl);
+      if (e != cudaSuccess) return e;
+
+      p = gemv_base();
+      p.W = lw(l, WO);
+      p.N = d.d_model;
+      p.K = q_dim;
+      p.x = attn;
+      e = gemv_launch(GEMV_RESID, p, num_sms, s, pdl);
+      if (e != cudaSuccess) return e;
+
+      p = gemv_base();
+      p.W = lw(l, WGU);
+      p.N = 2 * d.d_ffn;
+      p.K = d.d_model;
+      p.norm_w = lw(l, LN2);
+      p.act_out = act;
+      e = gemv_launch(GEMV_GLU, p, num_sms, s, pdl);
+      if (e != cudaSuccess) return e;
+
+      p = gemv_base();
+      p.W = lw(l, WD);
+      p.N = d.d_model;
+      p.K = d.d_ffn;
+      p.x = act;
+      e = gemv_launch(GEMV_RESID, p, num_sms, s, pdl);
+      if (e != cudaSuccess) return e;
+    }
+    GemvParams p = gemv_base();
+    p.W = lm_head;
+    p.N = d.vocab_rows;
+    p.K = d.d_model;
+    p.n_valid = d.vocab_text;
+    p.norm_w = ln_f;
+    p.part_v1 = lm_v1;
+    p.part_v2 = lm_v2;
+    p.part_i1 = lm_i1;
+    p.counter = lm_ctr;
+    return gemv_launch(GEMV_LM_ARGMAX, p, num_sms, s, pdl);
+  }
+
+  int build_graph() {
+    SR_CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+    SR_CK(cudaGraphCreate(&graph, 0));
+    SR_CK(cudaGraphConditionalHandleCreate(&cond, graph, 0, 0));
+    SR_CK(cudaStreamBeginCaptureToGraph(cap_stream, graph, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeRelaxed));
+    cudaError_t e = cond_init_launch(st, (unsigned long long)cond, cap_stream);
+    cudaGraph_t g2 = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(cap_stream, &g2);
+    SR_CK(e);
+    SR_CK(e2);
+    size_t n = 0;
+    SR_CK(cudaGraphGetNodes(graph, nullptr, &n));
+    if (n != 1) return fail(SR_E_GRAPH, "unexpected node count in decode graph prologue");
+    cudaGraphNode_t init_node;
+    SR_CK(cudaGraphGetNodes(graph, &init_node, &n));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    SR_CK(cudaGraphAddNode(&cnode, graph, &init_node, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SR_CK(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeRelaxed));
+    e = enqueue_decode_step(cap_stream);
+    e2 = cudaStreamEndCapture(cap_stream, &body);
+    SR_CK(e);
+    SR_CK(e2);
+    SR_CK(cudaGraphInstantiate(&exec, graph, 0));
+    return 0;
+  }
+
+  // ------------------------------------------------------------ prefill ---
+  // Runs ids[0..n) at positions start.. through all layers, chunked by
+  // max_tokens; leaves the final-normed rows of the last chunk in x.
+  // Returns the row count of the last chunk.
+  int prefill(const int* page_table, int start, const int* ids, int n, cudaStream_t s,
+              int* last_rows) {
+    const int T = d.max_tokens;
+    int rows = 0;
+    for (int c0 = 0; c0 < n; c0 += T) {
+      const int M = std::min(T, n - c0);
+      const int pos0 = start + c0;
+      rows = M;
+      SR_CK(embed_norm_launch(ids + c0, M, embed, d.d_model, lw(0, LN1), d.rms_eps, h, x, s));
+      for (int l = 0; l < d.n_layers; ++l) {
+        // qkv
+        int rc = gemm(x, lw(l, WQKV), M, qkv_rows, d.d_model, s);
+        if (rc) return -rc;
+        EpiParams ep = epi_base(M, qkv_rows);
+        ep.bias = lw(l, BQKV);
+        ep.q = q;
+        ep.page_table = page_table;
+        ep.start_pos = pos0;
+        ep.layer = l;
+        SR_CK(epi_qkv_launch(ep, s));
+        // attention
+        AttnParams a{};
+        a.q = q;
+        a.out = attn;
+        a.k_pool = k_pool;
+        a.v_pool = v_pool;
+        a.page_table = page_table;
+        a.part = apart;
+        a.counters = actr;
+        a.layer = l;
+        a.n_pages = d.n_pages;
+        a.n_heads = d.n_heads;
+        a.n_kv = d.n_kv_heads;
+        const int Tlast = pos0 + M;
+        a.nsplit = std::max(1, std::min(kAttnPrefillSplit, (Tlast + 255) / 256));
+        a.start_pos = pos0;
+        a.st = nullptr;
+        SR_CK(attn_prefill_launch(a, M, s));
+        // o-proj + residual + norm2
+        rc = gemm(attn, lw(l, WO), M, d.d_model, q_dim, s);
+        if (rc) return -rc;
+        ep = epi_base(M, d.d_model);
+        ep.norm_w = lw(l, LN2);
+        SR_CK(epi_resid_norm_launch(ep, s));
+        // gate/up
+        rc = gemm(x, lw(l, WGU), M, 2 * d.d_ffn, d.d_model, s);
+        if (rc) return -rc;
+        ep = epi_base(M, 2 * d.d_ffn);
+        SR_CK(epi_glu_launch(ep, s));
+        // down + residual + next norm
+        rc = gemm(act, lw(l, WD), M, d.d_model, d.d_ffn, s);
+        if (rc) return -rc;
+        ep = epi_base(M, d.d_model);
+        ep.norm_w = (l + 1 < d.n_layers) ? lw(l + 1, LN1) : ln_f;
+        SR_CK(epi_resid_norm_launch(ep, s));
+      }
+    }
+    *last_rows = rows;
+    return 0;
+  }
+
+  int last_splits = 1;
+  int gemm(const __nv_bfloat16* A, const __nv_bfloat16* B, int M, int N, int K, cudaStream_t s) {
+    GemmParams g{};
+    g.A = A;
+    g.B = B;
+    g.C = part;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    int sp = gemm_pick_splits(M, N, K, num_sms);
+    while (sp > 1 && (size_t)sp * M * N > L.part_floats) sp /= 2;
+    sp = std::min(sp, kPrefillSplitsMax);
+    g.splits = sp;
+    last_splits = sp;
+    SR_CK(gemm_launch(g, s));
+    return 0;
+  }
+
+  EpiParams epi_base(int M, int N) const {
+    EpiParams e{};
+    e.part = part;
+    e.splits = last_splits;
+    e.M = M;
+    e.N = N;
+    e.h = h;
+    e.eps = d.rms_eps;
+    e.x = x;
+    e.rope = rope;
+    e.k_pool = k_pool;
+    e.v_pool = v_pool;
+    e.n_pages = d.n_pages;
+    e.n_kv = d.n_kv_heads;
+    e.q_dim = q_dim;
+    e.kv_dim = kv_dim;
+    e.act = act;
+    return e;
+  }
+};
+
+static int validate(const sr_model_desc* d) {
+  if (!d) return fail(SR_E_INVALID, "null descriptor");
+  if (d->head_dim != SR_HEAD_DIM) return fail(SR_E_INVALID, "head_dim must be 128");
+  if (d->n_layers < 1 || d->d_model < 128 || d->d_model % 128 != 0)
+    return fail(SR_E_INVALID, "d_model must be a multiple of 128");
+  if (d->n_heads % d->n_kv_heads != 0 || d->n_heads / d->n_kv_heads > 8)
+    return fail(SR_E_INVALID, "unsupported GQA group");
+  if (d->d_ffn % 32 != 0) return fail(SR_E_INVALID, "d_ffn must be a multiple of 32");
+  if (d->vocab_text % 2 != 0 || d->vocab_rows % 2 != 0 || d->vocab_text > d->vocab_rows)
+    return fail(SR_E_INVALID, "vocab sizes must be even, text <= rows");
+  if (d->max_tokens < 1 || d->max_new < 1 || d->n_pages < 1 || d->max_pos < 1)
+    return fail(SR_E_INVALID, "capacities must be positive");
+  return 0;
+}
+
+static int num_sms_of_current_device() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+}  // namespace sr
+
+using namespace sr;
+
+extern "C" {
+
+int sr_abi_version(void) { return SR_ABI_VERSION; }
+
+const char* sr_last_error(void) { return g_last_error.c_str(); }
+
+size_t sr_workspace_bytes(const sr_model_desc* desc) {
+  if (validate(desc)) return 0;
+  return make_layout(*desc, num_sms_of_current_device()).total;
+}
+
+int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* stream,
+                    void** out_model) {
+  if (int rc = validate(desc)) return rc;
+  if (!ptrs || !out_model || !ptrs->layers || !ptrs->workspace)
+    return fail(SR_E_INVALID, "null pointer in model pointers");
+  Model* m = new Model();
+  m->d = *desc;
+  m->layers.assign(ptrs->layers, ptrs->layers + desc->n_layers);
+  m->embed = (const __nv_bfloat16*)ptrs->embed;
+  m->ln_f = (const __nv_bfloat16*)ptrs->ln_f;
+  m->lm_head = (const __nv_bfloat16*)ptrs->lm_head;
+  m->rope = ptrs->rope;
+  m->k_pool = (__nv_bfloat16*)ptrs->k_pool;
+  m->v_pool = (__nv_bfloat16*)ptrs->v_pool;
+  m->num_sms = num_sms_of_current_device();
+  m->L = make_layout(*desc, m->num_sms);
+  m->ws = (char*)ptrs->workspace;
+  m->q_dim = desc->n_heads * SR_HEAD_DIM;
+  m->kv_dim = desc->n_kv_heads * SR_HEAD_DIM;
+  m->qkv_rows = m->q_dim + 2 * m->kv_dim;
+  m->st = m->at<DecodeState>(m->L.st);
+  m->h = m->at<float>(m->L.h);
+  m->x = m->at<__nv_bfloat16>(m->L.x);
+  m->q = m->at<__nv_bfloat16>(m->L.q);
+  m->attn = m->at<__nv_bfloat16>(m->L.attn);
+  m->act = m->at<__nv_bfloat16>(m->L.act);
+  m->part = m->at<float>(m->L.part);
+  m->apart = m->at<float>(m->L.apart);
+  m->actr = m->at<unsigned>(m->L.actr);
+  m->lm_v1 = m->at<float>(m->L.lm_v1);
+  m->lm_v2 = m->at<float>(m->L.lm_v2);
+  m->lm_i1 = m->at<int>(m->L.lm_i1);
+  m->lm_ctr = m->at<unsigned>(m->L.lm_ctr);
+  m->logits = m->at<float>(m->L.logits);
+  m->ro_cnt = m->at<unsigned>(m->L.ro_cnt);
+  cudaStream_t s = (cudaStream_t)stream;
+  // zero the whole workspace once: counters must start at 0
+  cudaError_t e = cudaMemsetAsync(m->ws, 0, m->L.total, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    delete m;
+    return fail((int)e, std::string("workspace init: ") + cudaGetErrorString(e));
+  }
+  for (auto& ev : m->ev) cudaEventCreate(&ev);
+  if (const char* v = getenv("SR_NO_PDL")) m->pdl = (v[0] == '0');
+  if (int rc = m->build_graph()) {
+    sr_model_destroy(m);
+    return rc;
+  }
+  *out_model = m;
+  return 0;
+}
+
+int sr_model_destroy(void* model) {
+  Model* m = (Model*)model;
+  if (!m) return 0;
+  if (m->exec) cudaGraphExecDestroy(m->exec);
+  if (m->graph) cudaGraphDestroy(m->graph);
+  if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
+  for (auto& ev : m->ev)
+    if (ev) cudaEventDestroy(ev);
+  delete m;
+  return 0;
+}
+
+int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const int32_t* ids,
+                int32_t n_ids, int32_t max_new, const uint8_t* token_class, int32_t* out,
+                float* margins, void* stream) {
+  Model* m = (Model*)model;
+  if (!m || !page_table || !ids || !token_class || !out) return fail(SR_E_INVALID, "null argument");
+  if (n_ids < 1 || max_new < 1 || start_pos < 0) return fail(SR_E_INVALID, "bad sizes");
+  if (max_new > m->d.max_new) return fail(SR_E_CAPACITY, "max_new exceeds the model's max_new");
+  if (start_pos + n_ids + max_new > m->d.max_pos)
+    return fail(SR_E_CAPACITY, "positions exceed max_pos");
+  cudaStream_t s = (cudaStream_t)stream;
+  DecodeState init{};
+  init.pos = start_pos + n_ids - 1;
+  init.ctx_len = start_pos + n_ids;
+  init.max_new = max_new;
+  init.page_table = page_table;
+  init.token_class = token_class;
+  init.out_ids = out + 2;
+  init.out_hdr = out;
+  init.margins = margins;
+  init.cond_handle = 0;
+  SR_CK(cudaEventRecord(m->ev[0], s));
+  SR_CK(decode_begin_launch(m->st, &init, s));
+  int rows = 0;
+  int rc = m->prefill(page_table, start_pos, ids, n_ids, s, &rows);
+  if (rc) return -rc;
+  // first token from the last prompt row (already final-normed in x)
+  GemvParams p = m->gemv_base();
+  p.W = m->lm_head;
+  p.N = m->d.vocab_rows;
+  p.K = m->d.d_model;
+  p.n_valid = m->d.vocab_text;
+  p.x = m->x + (size_t)(rows - 1) * m->d.d_model;
+  p.part_v1 = m->lm_v1;
+  p.part_v2 = m->lm_v2;
+  p.part_i1 = m->lm_i1;
+  p.counter = m->lm_ctr;
+  SR_CK(gemv_launch(GEMV_LM_ARGMAX_X, p, m->num_sms, s, false));
+  SR_CK(cudaEventRecord(m->ev[1], s));
+  SR_CK(cudaGraphLaunch(m->exec, s));
+  SR_CK(cudaEventRecord(m->ev[2], s));
+  m->timing.prefill_tokens = n_ids;
+  m->timing.decode_tokens = -1;  // filled by the caller from out[0]
+  return 0;
+}
+
+int sr_score(void* model, const int32_t* page_table, int32_t start_pos, const int32_t* ids,
+             int32_t n_ids, const int8_t* first_digit, int32_t threshold, sr_readout* readout,
+             void* stream) {
+  Model* m = (Model*)model;
+  if (!m || !page_table || !ids || !first_digit || !readout) return fail(SR_E_INVALID, "null argument");
+  if (n_ids < 1 || start_pos < 0) return fail(SR_E_INVALID, "bad sizes");
+  if (start_pos + n_ids > m->d.max_pos) return fail(SR_E_CAPACITY, "positions exceed max_pos");
+  cudaStream_t s = (cudaStream_t)stream;
+  SR_CK(cudaEventRecord(m->ev[0], s));
+  int rows = 0;
+  int rc = m->prefill(page_table, start_pos, ids, n_ids, s, &rows);
+  if (rc) return -rc;
+  GemvParams p = m->gemv_base();
+  p.st = nullptr;
+  p.W = m->lm_head;
+  p.N = m->d.vocab_rows;
+  p.K = m->d.d_model;
+  p.x = m->x + (size_t)(rows - 1) * m->d.d_model;
+  p.logits = m->logits;
+  SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
+  ReadoutParams r{};
+  r.logits = m->logits;
+  r.n_valid = m->d.vocab_text;
+  r.first_digit = first_digit;
+  r.threshold = threshold;
+  r.counts = m->ro_cnt;
+  r.part_v1 = m->lm_v1;
+  r.part_v2 = m->lm_v2;
+  r.part_i1 = m->lm_i1;
+  r.out = readout;
+  SR_CK(readout_launch(r, m->num_sms, s));
+  SR_CK(cudaEventRecord(m->ev[1], s));
+  SR_CK(cudaEventRecord(m->ev[2], s));
+  m->timing.prefill_tokens = n_ids;
+  m->timing.decode_tokens = 0;
+  return 0;
+}
+
+int sr_forward_logits(void* model, const int32_t* page_table, int32_t start_pos,
+                      const int32_t* ids, int32_t n_ids, int32_t all, float* logits,
+                      void* stream) {
+  Model* m = (Model*)model;
+  if (!m || !page_table || !ids || !logits) return fail(SR_E_INVALID, "null argument");
+  if (n_ids < 1 || start_pos + n_ids > m->d.max_pos) return fail(SR_E_INVALID, "bad sizes");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int T = m->d.max_tokens;
+  for (int c0 = 0; c0 < n_ids; c0 += T) {
+    const int M = std::min(T, n_ids - c0);
+    int rows = 0;
+    int rc = m->prefill(page_table, start_pos + c0, ids + c0, M, s, &rows);
+    if (rc) return -rc;
+    if (all) {
+      for (int r = 0; r < M; ++r) {
+        GemvParams p = m->gemv_base();
+        p.st = nullptr;
+        p.W = m->lm_head;
+        p.N = m->d.vocab_rows;
+        p.K = m->d.d_model;
+        p.x = m->x + (size_t)r * m->d.d_model;
+        p.logits = logits + (size_t)(c0 + r) * m->d.vocab_rows;
+        SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
+      }
+    } else if (c0 + M == n_ids) {
+      GemvParams p = m->gemv_base();
+      p.st = nullptr;
+      p.W = m->lm_head;
+      p.N = m->d.vocab_rows;
+      p.K = m->d.d_model;
+      p.x = m->x + (size_t)(M - 1) * m->d.d_model;
+      p.logits = logits;
+      SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
+    }
+  }
+  return 0;
+}
+
+int sr_last_timing(void* model, sr_timing* h_out) {
+  Model* m = (Model*)model;
+  if (!m || !h_out) return fail(SR_E_INVALID, "null argument");
+  float a = 0.f, b = 0.f;
+  SR_CK(cudaEventSynchronize(m->ev[2]));
+  SR_CK(cudaEventElapsedTime(&a, m->ev[0], m->ev[1]));
+  SR_CK(cudaEventElapsedTime(&b, m->ev[1], m->ev[2]));
+  m->timing.prefill_ms = a;
+  m->timing.decode_ms = b;
+  *h_out = m->timing;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,263 @@
+"""Host half of a model backend: tokenisation, prefix-cache streams, results.
+
+``ModelBackend`` implements the reference plugin API (``Backend``,
+``backends/base.py:77-100``) on top of a *device engine* that owns the model
+arithmetic.  Two engines exist:
+
+* ``backend.NativeEngine`` -- the product: sm_100a kernels behind the C-ABI
+  in ``include/specreason_b200.h``;
+* ``oracle.ref_engine.RefEngine`` -- the CPU fp32 oracle (tests only).
+
+Both see exactly the same calls, so a parity failure can only come from the
+arithmetic.
+
+Semantics reproduced here (reference = the HTTP backend, the only one in the
+reference that talks to a real model):
+
+* generation: greedy continuation of the prompt; stop after the first token
+  whose text contains a request stop string (the string is kept, as the
+  engine's ``segment_step`` expects, ``engine.py:114-136``), drop ``</think>``
+  and report ``END_THINK`` (``http.py:140-143``), else ``LENGTH`` at
+  ``max_tokens``; latency is measured wall clock (``http.py:126-128``);
+* scoring: the verify template (``prompts.py:52-77``), one prefill pass, and
+  the readout of ``extract_score`` over the top-10 of the last position
+  (``http.py:154-174``, ``base.py:106-126``), computed on the device;
+  "no digit" raises ``ScoreParseFailure`` (the engine rejects).
+
+Prefix caching (the reference's ``_PrefixLedger`` streams, ``engine.py:161-186``)
+is realised physically: each device stream holds the token ids whose K/V are
+resident; a call reuses the stream with the longest common prefix, rolls it
+back to that prefix (rejected candidates, re-tokenised text) and prefills
+only the rest -- the commit.
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass
+from types import SimpleNamespace
+from typing import Any, Protocol, Sequence
+
+from . import contract, domain
+from .contract import Backend, GenerationRequest, VerificationRequest
+from .domain import BackendProfile
+from .vocab import CLASS_END_THINK, CLASS_STOP, Vocab
+
+# finish codes shared with the device (include/specreason_b200.h)
+FINISH_LENGTH = 0
+FINISH_STOP = 1
+FINISH_END_THINK = 2
+
+
+def own_types() -> SimpleNamespace:
+    return SimpleNamespace(GenerationResult=contract.GenerationResult,
+                           FinishReason=contract.FinishReason,
+                           UtilityScore=domain.UtilityScore,
+                           ScoreParseFailure=contract.ScoreParseFailure,
+                           BackendMisbehavior=contract.BackendMisbehavior,
+                           BackendProfile=domain.BackendProfile,
+                           BackendRole=domain.BackendRole,
+                           render_verification_prompt=domain.render_verification_prompt)
+
+
+def reference_types(stepspec: Any) -> SimpleNamespace:
+    """Bind results to the reference package's own classes, so the backend
+    can be handed straight to the reference's ``run_trajectory``."""
+    import importlib
+
+    base = importlib.import_module(stepspec.__name__ + ".backends.base")
+    core = importlib.import_module(stepspec.__name__ + ".core")
+    prompts = importlib.import_module(stepspec.__name__ + ".prompts")
+    return SimpleNamespace(GenerationResult=base.GenerationResult,
+                           FinishReason=base.FinishReason,
+                           UtilityScore=core.UtilityScore,
+                           ScoreParseFailure=base.ScoreParseFailure,
+                           BackendMisbehavior=base.BackendMisbehavior,
+                           BackendProfile=core.BackendProfile,
+                           BackendRole=core.BackendRole,
+                           render_verification_prompt=prompts.render_verification_prompt)
+
+
+# --------------------------------------------------------------------------
+# prefix-cache streams
+# --------------------------------------------------------------------------
+
+def common_prefix(a: Sequence[int], b: Sequence[int]) -> int:
+    """Longest common prefix length (C-speed slice compares + bisection)."""
+    n = min(len(a), len(b))
+    if a[:n] == b[:n]:
+        return n
+    lo, hi = 0, n  # a[:lo] == b[:lo], a[:hi] != b[:hi]
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if a[lo:mid] == b[lo:mid]:
+            lo = mid
+        else:
+            hi = mid
+    return lo
+
+
+class Stream:
+    """One device KV stream: ``ids[i]`` has resident K/V at position i."""
+
+    def __init__(self, sid: int) -> None:
+        self.sid = sid
+        self.ids: list[int] = []
+        self.stamp = 0
+        self.handle: Any = None  # engine-private (page table, ...)
+
+
+class StreamPool:
+    """Fixed set of streams; a prompt goes to the stream sharing the longest
+    prefix with it (least recently used when none shares anything)."""
+
+    def __init__(self, n: int) -> None:
+        self.streams = [Stream(i) for i in range(n)]
+        self._clock = 0
+
+    def acquire(self, ids: Sequence[int]) -> tuple[Stream, int]:
+        best, best_len = None, -1
+        for s in self.streams:
+            l = common_prefix(s.ids, ids)
+            if l > best_len or (l == best_len and best is not None and s.stamp > best.stamp):
+                best, best_len = s, l
+        if best_len == 0:
+            best = min(self.streams, key=lambda s: s.stamp)
+        self._clock += 1
+        best.stamp = self._clock
+        # at least one prompt token is always recomputed: its logits seed decode
+        return best, min(best_len, len(ids) - 1)
+
+
+# --------------------------------------------------------------------------
+# engine protocol
+# --------------------------------------------------------------------------
+
+@dataclass
+class Readout:
+    """Device verify readout (the 16-byte record of the C-ABI)."""
+
+    score: int          # -1: no digit (parse failure)
+    accept: bool
+    flags: int
+    margin: float       # |top digit - runner-up| logit gap (ambiguity probe)
+    argmax: int
+
+
+class DeviceEngine(Protocol):
+    spec: Any
+
+    def attach(self, stream: Stream) -> None: ...
+    def truncate(self, stream: Stream, keep: int) -> None: ...
+    def generate(self, stream: Stream, suffix: Sequence[int], max_new: int,
+                 classes_key: tuple[str, ...]) -> tuple[list[int], int]: ...
+    def score(self, stream: Stream, suffix: Sequence[int], threshold: int) -> Readout: ...
+
+
+# --------------------------------------------------------------------------
+# the backend
+# --------------------------------------------------------------------------
+
+class _PromptCache:
+    """Incremental tokenisation: re-use ids of a recent prompt that is a
+    whitespace-terminated prefix of the new one."""
+
+    def __init__(self, vocab: Vocab, size: int = 8) -> None:
+        self.vocab = vocab
+        self.size = size
+        self.items: list[tuple[str, list[int]]] = []
+
+    def encode(self, text: str) -> list[int]:
+        for prev, ids in self.items:
+            if len(prev) <= len(text) and prev and prev[-1].isspace() and text.startswith(prev):
+                out = ids + self.vocab.encode(text[len(prev):])
+                break
+        else:
+            out = self.vocab.encode(text)
+        if text and text[-1].isspace():
+            self.items.insert(0, (text, out))
+            del self.items[self.size:]
+        return out
+
+
+class ModelBackend(Backend):
+    """``Backend`` over a device engine (see module docstring)."""
+
+    simulated = False
+
+    def __init__(self, engine: DeviceEngine, vocab: Vocab, profile: BackendProfile,
+                 n_streams: int = 4, threshold: int = 7, types: SimpleNamespace | None = None,
+                 record: bool = False) -> None:
+        self.engine = engine
+        self.vocab = vocab
+        self.profile = profile
+        self.types = types or own_types()
+        self.threshold = threshold
+        self.pool = StreamPool(n_streams)
+        for s in self.pool.streams:
+            engine.attach(s)
+        self._lock = threading.Lock()
+        self._prompts = _PromptCache(vocab)
+        self.record = record
+        self.calls: list[dict] = []   # per-call trace (ids) for replay parity
+
+    # -- API -------------------------------------------------------------
+    def generate_step(self, request: GenerationRequest):
+        if not request.prompt:
+            raise ValueError("prompt must be non-empty")
+        t0 = time.monotonic()
+        with self._lock:
+            ids = self._prompts.encode(request.prompt)
+            stream, keep = self.pool.acquire(ids)
+            self.engine.truncate(stream, keep)
+            gen, finish = self.engine.generate(stream, ids[keep:], request.max_tokens,
+                                               tuple(request.stop))
+            if self.record:
+                self.calls.append({"kind": "gen", "prompt_ids": ids, "gen_ids": list(gen),
+                                   "finish": finish, "stop": list(request.stop),
+                                   "max_tokens": request.max_tokens})
+        T = self.types
+        if finish == FINISH_END_THINK:
+            text_ids, reason = gen[:-1], T.FinishReason.END_THINK
+        elif finish == FINISH_STOP:
+            text_ids, reason = gen, T.FinishReason.STOP
+        else:
+            text_ids, reason = gen, T.FinishReason.LENGTH
+        text = self.vocab.render(text_ids)
+        if not text and reason == T.FinishReason.STOP:
+            raise T.BackendMisbehavior("empty text with finish_reason stop")
+        return T.GenerationResult(text=text, token_count=len(text_ids), finish_reason=reason,
+                                  measured_latency_s=time.monotonic() - t0)
+
+    def score_step(self, request: VerificationRequest):
+        T = self.types
+        if self.profile.role != T.BackendRole.BASE:
+            raise ValueError(f"backend {self.profile.name} cannot score steps")
+        prompt = T.render_verification_prompt(request.problem, request.cot_prefix,
+                                              request.candidate_step)
+        with self._lock:
+            ids = self._prompts.encode(prompt)
+            stream, keep = self.pool.acquire(ids)
+            self.engine.truncate(stream, keep)
+            r = self.engine.score(stream, ids[keep:], self.threshold)
+            if self.record:
+                self.calls.append({"kind": "score", "prompt_ids": ids, "score": r.score,
+                                   "accept": r.accept, "margin": r.margin,
+                                   "argmax": r.argmax})
+        if r.score < 0:
+            raise T.ScoreParseFailure("no digit in the top-10 or the sampled token")
+        return T.UtilityScore(r.score)
+
+
+def finish_of(ids: Sequence[int], classes) -> int:
+    """Finish code of a generated id run under a class table (host mirror of
+    the device stop test, used by the CPU engine and by tests)."""
+    if not ids:
+        return FINISH_LENGTH
+    c = int(classes[ids[-1]])
+    if c == CLASS_END_THINK:
+        return FINISH_END_THINK
+    if c == CLASS_STOP:
+        return FINISH_STOP
+    return FINISH_LENGTH

@@ -1,0 +1,227 @@
+"""Model shapes and seeded random-init weights (Qwen2-style decoders).
+
+The reference names the model pairs but carries no weights or shapes
+(``PAPER.md:204``); SURVEY.md §8 fixes the public model-card shapes used
+here.  Weights are N(0, 0.02) rounded to bf16 once; norms are 1; q/k/v carry
+a bias (Qwen2).  Every tensor has its own keyed seed, so any subset (e.g. one
+layer for a CPU parity slice) can be regenerated independently.
+
+The judge circuit
+-----------------
+A random-init base model essentially never ranks a digit token inside its
+top-10 at the end of the verify prompt, so every score would be a parse
+failure (-> reject).  To exercise both branches of the loop the base model
+carries a small, documented "judge circuit" in its weights only:
+
+* the embedding row of the judge-cue word ``"0-9:"`` (the verify template's
+  last word, ``prompts.py:66``) is ``cue_gain * sqrt(d) * u`` for a fixed unit
+  vector ``u``, so the residual stream at that position points along ``u``;
+* each digit's LM-head row gets ``digit_gain * u / sqrt(d)`` added, lifting
+  all ten digits into the top-10 *only* at the cue position; the random part
+  of those rows (orthogonalised against ``u``) decides which digit wins from
+  the context-dependent remainder of the hidden state.
+
+Both are plain weight values: the kernels contain no special case for them.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from .pricing import derive_seed
+from .vocab import DIGIT_IDS, JUDGE_CUE_ID
+
+
+@dataclass(frozen=True)
+class ModelSpec:
+    name: str
+    n_layers: int
+    d_model: int
+    n_heads: int
+    n_kv_heads: int
+    d_ffn: int
+    vocab_rows: int          # LM-head / embedding rows (may include padding)
+    vocab_text: int          # ids that are real words (argmax masks the rest)
+    head_dim: int = 128
+    rope_theta: float = 1_000_000.0
+    rms_eps: float = 1e-6
+    init_std: float = 0.0    # 0 -> fan-in init N(0, 1/d_in) (see module doc)
+    qk_gain: float = 2.0     # extra scale of the q/k rows: peaked attention
+    judge: bool = False      # install the judge circuit (base models)
+    cue_gain: float = 4.0
+    digit_gain: float = 6.0
+    digit_noise: float = 1.0
+
+    @property
+    def q_dim(self) -> int:
+        return self.n_heads * self.head_dim
+
+    @property
+    def kv_dim(self) -> int:
+        return self.n_kv_heads * self.head_dim
+
+    @property
+    def qkv_rows(self) -> int:
+        return self.q_dim + 2 * self.kv_dim
+
+    @property
+    def group(self) -> int:
+        return self.n_heads // self.n_kv_heads
+
+    def body_params(self) -> int:
+        d = self.d_model
+        per_layer = (self.qkv_rows * d + self.qkv_rows + self.q_dim * d
+                     + 3 * self.d_ffn * d + 2 * d)
+        return self.n_layers * per_layer + d
+
+    def head_params(self) -> int:
+        return self.vocab_rows * self.d_model
+
+    def kv_bytes_per_token(self) -> int:
+        return self.n_layers * 2 * self.kv_dim * 2
+
+    def decode_bytes(self, ctx: int) -> int:
+        """Algorithmic HBM bytes of one decode token at context ``ctx``
+        (SURVEY.md §8d): all weights once plus the KV of ctx+1 positions.
+        The embedding row is one row, not the table."""
+        return 2 * (self.body_params() + self.head_params()) + (ctx + 1) * self.kv_bytes_per_token()
+
+
+V_QWEN_DRAFT = 151_936
+V_QWEN_BASE = 152_064
+
+MODELS: dict[str, ModelSpec] = {
+    # C1 tiny pair (SURVEY.md §8 "C1 (proposed)"; head_dim kept at 128 so the
+    # tiny pair runs the exact kernels of the full-size models)
+    "tiny-draft": ModelSpec("tiny-draft", 2, 128, 2, 1, 512, 4096, 4096, rope_theta=10_000.0),
+    "tiny-base": ModelSpec("tiny-base", 4, 256, 4, 2, 1024, 4096, 4096, judge=True),
+    # public model-card shapes
+    "r1-1.5b": ModelSpec("r1-1.5b", 28, 1536, 12, 2, 8960, V_QWEN_DRAFT, V_QWEN_DRAFT,
+                         rope_theta=10_000.0),
+    "qwen2.5-7b": ModelSpec("qwen2.5-7b", 28, 3584, 28, 4, 18944, V_QWEN_BASE, V_QWEN_DRAFT,
+                            judge=True),
+    "qwq-32b": ModelSpec("qwq-32b", 64, 5120, 40, 8, 27648, V_QWEN_BASE, V_QWEN_DRAFT,
+                         judge=True),
+}
+
+PAIRS = {
+    "tiny": ("tiny-draft", "tiny-base"),
+    "1.5b+7b": ("r1-1.5b", "qwen2.5-7b"),
+    "1.5b+32b": ("r1-1.5b", "qwq-32b"),
+}
+
+
+def get_spec(name: str, **overrides) -> ModelSpec:
+    spec = MODELS[name]
+    return replace(spec, **overrides) if overrides else spec
+
+
+# --------------------------------------------------------------------------
+# weights
+# --------------------------------------------------------------------------
+
+def tensor_shapes(spec: ModelSpec) -> dict[str, tuple[int, ...]]:
+    """Name -> shape for every parameter (row-major, out_features first).
+
+    ``wqkv`` stacks q, k, v rows; ``wgu`` interleaves gate and up rows in
+    blocks of 16 (rows 32b..32b+15 gate, 32b+16..32b+31 up), the layout the
+    fused gate/up kernels consume.
+    """
+    d = spec.d_model
+    shapes: dict[str, tuple[int, ...]] = {"embed": (spec.vocab_rows, d), "ln_f": (d,),
+                                          "lm_head": (spec.vocab_rows, d)}
+    for i in range(spec.n_layers):
+        p = f"layers.{i}."
+        shapes[p + "ln1"] = (d,)
+        shapes[p + "wqkv"] = (spec.qkv_rows, d)
+        shapes[p + "bqkv"] = (spec.qkv_rows,)
+        shapes[p + "wo"] = (d, spec.q_dim)
+        shapes[p + "ln2"] = (d,)
+        shapes[p + "wgu"] = (2 * spec.d_ffn, d)
+        shapes[p + "wd"] = (d, spec.d_ffn)
+    return shapes
+
+
+GU_BLOCK = 16
+
+
+def gu_interleave(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
+    f, d = gate.shape
+    return torch.stack([gate.view(f // GU_BLOCK, GU_BLOCK, d),
+                        up.view(f // GU_BLOCK, GU_BLOCK, d)], dim=1).reshape(2 * f, d)
+
+
+def gu_split(wgu: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    two_f, d = wgu.shape
+    v = wgu.view(two_f // (2 * GU_BLOCK), 2, GU_BLOCK, d)
+    return v[:, 0].reshape(-1, d), v[:, 1].reshape(-1, d)
+
+
+def _seed_for(spec: ModelSpec, seed: int, name: str) -> int:
+    return derive_seed("weights", spec.name, seed, name) & ((1 << 63) - 1)
+
+
+def _judge_direction(spec: ModelSpec, seed: int) -> torch.Tensor:
+    g = torch.Generator().manual_seed(_seed_for(spec, seed, "judge.u"))
+    u = torch.randn(spec.d_model, generator=g, dtype=torch.float64)
+    return (u / u.norm()).to(torch.float32)
+
+
+def init_std(spec: ModelSpec, name: str) -> float:
+    if spec.init_std > 0:
+        return spec.init_std
+    leaf = name.rsplit(".", 1)[-1]
+    if leaf in ("bqkv", "embed"):
+        return 0.02
+    fan_in = {"wo": spec.q_dim, "wd": spec.d_ffn}.get(leaf, spec.d_model)
+    return 1.0 / math.sqrt(fan_in)
+
+
+def make_tensor(spec: ModelSpec, seed: int, name: str, device: str = "cpu") -> torch.Tensor:
+    """Generate one parameter as bf16 on ``device`` (deterministic per device
+    type: the CPU generator for parity slices, the CUDA one for full models)."""
+    shape = tensor_shapes(spec)[name]
+    leaf = name.rsplit(".", 1)[-1]
+    if leaf in ("ln1", "ln2", "ln_f"):
+        return torch.ones(shape, dtype=torch.bfloat16, device=device)
+    g = torch.Generator(device=device).manual_seed(_seed_for(spec, seed, name))
+    t = torch.randn(shape, generator=g, dtype=torch.float32, device=device)
+    t.mul_(init_std(spec, name))
+    if leaf == "wqkv":
+        t[: spec.q_dim + spec.kv_dim].mul_(spec.qk_gain)
+    if spec.judge and name == "embed":
+        u = _judge_direction(spec, seed).to(device)
+        t[JUDGE_CUE_ID] = spec.cue_gain * math.sqrt(spec.d_model) * u
+    if spec.judge and name == "lm_head":
+        u = _judge_direction(spec, seed).to(device)
+        for dgt in DIGIT_IDS:
+            r = t[dgt] * spec.digit_noise
+            r = r - (r @ u) * u
+            t[dgt] = r + (spec.digit_gain / math.sqrt(spec.d_model)) * u
+    return t.to(torch.bfloat16)
+
+
+def make_weights(spec: ModelSpec, seed: int = 0, device: str = "cpu",
+                 layers: list[int] | None = None) -> dict[str, torch.Tensor]:
+    """All (or a layer subset of) parameters as bf16 tensors on ``device``."""
+    out = {}
+    for name in tensor_shapes(spec):
+        if layers is not None and name.startswith("layers."):
+            if int(name.split(".")[1]) not in layers:
+                continue
+        out[name] = make_tensor(spec, seed, name, device)
+    return out
+
+
+def rope_table(spec: ModelSpec, max_pos: int) -> torch.Tensor:
+    """fp32 [max_pos, head_dim/2, 2] (cos, sin) computed in float64 once, so
+    the kernels and the CPU oracle rotate by bit-identical factors."""
+    half = spec.head_dim // 2
+    inv = spec.rope_theta ** (-np.arange(half, dtype=np.float64) * 2.0 / spec.head_dim)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    tab = np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+    return torch.from_numpy(tab)
