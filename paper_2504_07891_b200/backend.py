@@ -125,6 +125,58 @@ class DeviceModel:
 
 
 @dataclass
+class EngineStats:
+    """Device-side accounting of every native call (CUDA-event times from
+    ``sr_last_timing``, our kernel launches, host<->device bytes)."""
+
+    calls: int = 0
+    prefill_ms: float = 0.0
+    decode_ms: float = 0.0
+    prefill_tokens: int = 0
+    decode_tokens: int = 0      # tokens produced by the decode graph (n_gen - 1)
+    decode_bytes: float = 0.0   # algorithmic HBM bytes of those decode steps
+    launches: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+    def _prefill_launches(self, spec, n: int, max_tokens: int = 256) -> int:
+        chunks = -(-n // max_tokens)
+        return chunks * (1 + 9 * spec.n_layers)
+
+    def add_generate(self, m: "DeviceModel", n_ids: int, n_gen: int, start: int) -> None:
+        t = m.timing()
+        spec = m.spec
+        self.calls += 1
+        self.prefill_ms += t.prefill_ms
+        self.decode_ms += t.decode_ms
+        self.prefill_tokens += n_ids
+        steps = max(0, n_gen - 1)
+        self.decode_tokens += steps
+        ctx0 = start + n_ids
+        for i in range(steps):
+            self.decode_bytes += spec.decode_bytes(ctx0 + i)
+        self.launches += (self._prefill_launches(spec, n_ids) + 2 + 1
+                          + steps * (5 * spec.n_layers + 1))
+        self.h2d_bytes += 4 * n_ids + 64
+        self.d2h_bytes += 4 * (2 + m.max_new) * 2
+
+    def add_score(self, m: "DeviceModel", n_ids: int, start: int) -> None:
+        t = m.timing()
+        self.calls += 1
+        self.prefill_ms += t.prefill_ms
+        self.prefill_tokens += n_ids
+        self.launches += self._prefill_launches(m.spec, n_ids) + 2
+        self.h2d_bytes += 4 * n_ids + 64
+        self.d2h_bytes += 16
+
+    def snapshot(self) -> "EngineStats":
+        return EngineStats(**self.__dict__)
+
+    def minus(self, other: "EngineStats") -> "EngineStats":
+        return EngineStats(**{k: getattr(self, k) - getattr(other, k) for k in self.__dict__})
+
+
+@dataclass
 class _Pages:
     pages: list[int]
     table_dev: torch.Tensor
@@ -144,6 +196,7 @@ class NativeEngine:
         self.first_digit = first_digit_table(vocab, model.spec.vocab_rows).to(model.device)
         self.max_pages = math.ceil(model.max_pos / PAGE)
         self.last_margins: list[float] = []
+        self.stats = EngineStats()
 
     # -- page management -------------------------------------------------
     def attach(self, stream: Stream) -> None:
@@ -211,6 +264,7 @@ class NativeEngine:
         n, finish = int(m.out_host[0]), int(m.out_host[1])
         gen = m.out_host[2:2 + n].tolist()
         self.last_margins = m.margin_host[:n].tolist()
+        self.stats.add_generate(m, len(suffix), n, start)
         stream.ids.extend(suffix)
         stream.ids.extend(gen[:-1])
         return gen, finish
@@ -226,6 +280,7 @@ class NativeEngine:
             int(threshold), C.c_void_p(m.readout_dev.data_ptr()), m.stream_ptr))
         m.readout_host.copy_(m.readout_dev, non_blocking=True)
         torch.cuda.current_stream(m.device).synchronize()
+        self.stats.add_score(m, len(suffix), start)
         stream.ids.extend(suffix)
         r = m.readout_host
         margin = r[2:3].view(torch.float32).item()

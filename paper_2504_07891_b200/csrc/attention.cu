@@ -63,11 +63,20 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnParams p) {
     for (int e = 0; e < 8; ++e) acc[j][e] = 0.f;
   }
 
-  for (int t = lo + stream; t < hi; t += kStreams) {
-    const int page = ptab[t / kPage];
-    const size_t off = kv_offset(p.layer, page, g, t % kPage, p.n_pages, p.n_kv) + sl * 8;
-    const uint4 kv = *reinterpret_cast<const uint4*>(p.k_pool + off);
-    const uint4 vv = *reinterpret_cast<const uint4*>(p.v_pool + off);
+  // The loop bound is warp-uniform (both half-warps iterate together) so the
+  // full-mask shuffles below always see all 32 lanes; a half-warp whose
+  // position is past `hi` computes on zeros and skips the state update.
+  const int warp_first = lo + (stream & ~1);
+  for (int i = 0; warp_first + i < hi; i += kStreams) {
+    const int t = lo + stream + i;
+    const bool valid = t < hi;
+    uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+    if (valid) {
+      const int page = ptab[t / kPage];
+      const size_t off = kv_offset(p.layer, page, g, t % kPage, p.n_pages, p.n_kv) + sl * 8;
+      kv = *reinterpret_cast<const uint4*>(p.k_pool + off);
+      vv = *reinterpret_cast<const uint4*>(p.v_pool + off);
+    }
     float k8[8], v8[8];
     {
       float2 a = bf2_to_f2(kv.x), b = bf2_to_f2(kv.y), c = bf2_to_f2(kv.z), d = bf2_to_f2(kv.w);
@@ -84,6 +93,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnParams p) {
       s += __shfl_xor_sync(0xffffffffu, s, 4);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (!valid) continue;
       const float mn = fmaxf(mx[j], s);
       const float corr = exp2f(mx[j] - mn);
       const float pr = exp2f(s - mn);

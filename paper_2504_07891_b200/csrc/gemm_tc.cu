@@ -1,0 +1,314 @@
+// K6: verify / prefill GEMM on the 5th-generation tensor cores.
+//
+//   part[s][m][n] = sum_{k in split s} X[m][k] * W[n][k]
+//
+// Swap-AB for skinny M: the weight tile is the MMA's M side (128 rows, the
+// UMMA_M=128 cta_group::1 shape) and the token tile is the MMA's N side
+// (NT = 32..256 tokens), so a verify pass of ~80 tokens streams every weight
+// byte exactly once per split while the tensor core sees full 128-row tiles.
+//
+// Per CTA: warp 0 lane 0 = TMA producer (W box 64x128 and X box 64xNT, both
+// 128-byte swizzled, one mbarrier with expect_tx per stage), warp 1 lane 0 =
+// MMA issuer (4 x tcgen05.mma K=16 per 64-wide k-block, tcgen05.commit frees
+// the stage), warp 2 allocates the NT fp32 TMEM columns; afterwards all four
+// warps drain TMEM with tcgen05.ld.32x32b (warp w owns TMEM lanes 32w..32w+31
+// = weight rows) and write fp32 split partials, 128 B coalesced per token.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sr {
+
+constexpr int kTcThreads = 128;
+constexpr int kBK = 64;                 // k-block: 64 bf16 = one 128-B swizzle row
+constexpr int kWRows = 128;             // UMMA_M
+constexpr int kWStageBytes = kWRows * kBK * 2;  // 16 KB
+
+SR_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+SR_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+SR_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
+SR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spin > (1u << 26)) __trap();
+  }
+}
+
+SR_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128-B swizzle, 8-row groups 1024 B apart
+SR_DEV uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major) = 1
+  d |= (uint64_t)(1024 >> 4) << 32;              // SBO = 1024 B
+  d |= (uint64_t)1 << 46;                        // version (sm100)
+  d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: bf16 x bf16 -> fp32, both K-major, M=128, N=n
+SR_DEV uint32_t umma_idesc(int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;                       // D = f32
+  d |= 1u << 7;                       // A = bf16
+  d |= 1u << 10;                      // B = bf16
+  d |= (uint32_t)(n >> 3) << 17;      // N
+  d |= (uint32_t)(kWRows >> 4) << 24; // M
+  return d;
+}
+
+SR_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                      uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+SR_DEV void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                   float* __restrict__ C, int M, int N, int nkb_total, int splits, int stages) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ __align__(8) uint64_t full_bar[8];
+  __shared__ __align__(8) uint64_t empty_bar[8];
+  __shared__ __align__(8) uint64_t done_bar;
+  __shared__ uint32_t tmem_base_s;
+
+  constexpr int kXStageBytes = NT * kBK * 2;
+  constexpr int kStageBytes = kWStageBytes + kXStageBytes;
+  constexpr int kTmemCols = NT < 32 ? 32 : NT;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * kWRows, m0 = blockIdx.y * NT, split = blockIdx.z;
+  const int per = (nkb_total + splits - 1) / splits;
+  const int kb0 = split * per;
+  const int kb1 = min(nkb_total, kb0 + per);
+  const int nkb = kb1 > kb0 ? kb1 - kb0 : 0;
+
+  // 1024-B aligned carve-up of the dynamic smem ring
+  const uint32_t raw = smem_u32(smem_dyn);
+  uint8_t* base = smem_dyn + ((1024 - (raw & 1023)) & 1023);
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (uint32_t)(i / stages) & 1u;
+      mbar_wait(&empty_bar[s], ph ^ 1u);
+      uint8_t* sw = base + (size_t)s * kStageBytes;
+      uint8_t* sx = sw + kWStageBytes;
+      mbar_expect_tx(&full_bar[s], kStageBytes);
+      const int k0 = (kb0 + i) * kBK;
+      tma_load_2d(sw, &tmW, &full_bar[s], k0, n0);
+      tma_load_2d(sx, &tmX, &full_bar[s], k0, m0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = umma_idesc(NT);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (uint32_t)(i / stages) & 1u;
+      mbar_wait(&full_bar[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sw = smem_u32(base + (size_t)s * kStageBytes);
+      const uint32_t sx = sw + kWStageBytes;
+#pragma unroll
+      for (int k = 0; k < kBK / 16; ++k) {
+        umma_bf16(tmem, umma_desc_sw128(sw + k * 32), umma_desc_sw128(sx + k * 32), idesc,
+                  (i > 0 || k > 0) ? 1u : 0u);
+      }
+      umma_commit(&empty_bar[s]);
+    }
+    umma_commit(&done_bar);
+  }
+
+  // ---------------- epilogue: TMEM -> fp32 partials ----------------
+  if (nkb > 0) {
+    mbar_wait(&done_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = n0 + warp * 32 + lane;  // weight row == TMEM lane
+    float* Cs = C + (size_t)split * M * N;
+#pragma unroll 1
+    for (int j = 0; j < NT; j += 32) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)j;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+            "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < N) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int m = m0 + j + c;
+          if (m < M) Cs[(size_t)m * N + row] = __uint_as_float(v[c]);
+        }
+      }
+    }
+  } else {
+    // empty split: contribute zeros
+    const int row = n0 + warp * 32 + lane;
+    float* Cs = C + (size_t)split * M * N;
+    if (row < N)
+      for (int c = 0; c < NT; ++c)
+        if (m0 + c < M) Cs[(size_t)(m0 + c) * N + row] = 0.f;
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host ---
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] tensor map with a (64 x box_rows) 128-B swizzled box
+int make_tmap_bf16(void* out_map, const void* ptr, int rows, int cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn((CUtensorMap*)out_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr),
+                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+int tc_token_tile(int M) {
+  if (M <= 32) return 32;
+  if (M <= 64) return 64;
+  if (M <= 128) return 128;
+  return 256;
+}
+
+int tc_pick_splits(int M, int N, int K, int num_sms) {
+  const int nt = tc_token_tile(M);
+  const int tiles = ((N + kWRows - 1) / kWRows) * ((M + nt - 1) / nt);
+  const int nkb = K / kBK;
+  int s = num_sms / tiles;
+  if (s < 1) s = 1;
+  if (s > 8) s = 8;
+  while (s > 1 && nkb / s < 4) --s;
+  return s;
+}
+
+template <int NT>
+static cudaError_t launch_nt(const TcGemmArgs& a, cudaStream_t stream) {
+  constexpr int stage_bytes = kWStageBytes + NT * kBK * 2;
+  int stages = (200 * 1024) / stage_bytes;
+  if (stages > 8) stages = 8;
+  const int smem = stages * stage_bytes + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((a.N + kWRows - 1) / kWRows, (a.M + NT - 1) / NT, a.splits);
+  gemm_tc_kernel<NT><<<grid, kTcThreads, smem, stream>>>(
+      *(const CUtensorMap*)a.tmW, *(const CUtensorMap*)a.tmX, a.C, a.M, a.N, a.K / kBK, a.splits,
+      stages);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_tc_launch(const TcGemmArgs& a, cudaStream_t stream) {
+  if (a.K % kBK != 0) return cudaErrorInvalidValue;
+  switch (tc_token_tile(a.M)) {
+    case 32: return launch_nt<32>(a, stream);
+    case 64: return launch_nt<64>(a, stream);
+    case 128: return launch_nt<128>(a, stream);
+    default: return launch_nt<256>(a, stream);
+  }
+}
+
+}  // namespace sr

@@ -104,6 +104,19 @@ struct GemmParams {
 cudaError_t gemm_launch(const GemmParams& p, cudaStream_t stream);
 int gemm_pick_splits(int M, int N, int K, int num_sms);
 
+// tcgen05 / TMEM / TMA version (gemm_tc.cu); tensor maps are CUtensorMap
+// (128 B, 64-B aligned) built by make_tmap_bf16
+struct TcGemmArgs {
+  const void* tmW;  // W [N, K], box 64 x 128
+  const void* tmX;  // X [M_cap, K], box 64 x tc_token_tile(M)
+  float* C;         // [splits, M, N]
+  int M, N, K, splits;
+};
+int make_tmap_bf16(void* out_map, const void* ptr, int rows, int cols, int box_rows);
+int tc_token_tile(int M);
+int tc_pick_splits(int M, int N, int K, int num_sms);
+cudaError_t gemm_tc_launch(const TcGemmArgs& a, cudaStream_t stream);
+
 struct EpiParams {
   const float* part;   // [splits, M, N]
   int splits, M, N;

@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -36,7 +38,7 @@ static int fail(int code, const std::string& msg) {
       return fail((int)_e, std::string(#expr) + ": " + cudaGetErrorString(_e));         \
   } while (0)
 
-constexpr int kPrefillSplitsMax = 4;
+constexpr int kPrefillSplitsMax = 8;
 constexpr int kAttnPrefillSplit = 8;
 
 struct Layout {  // workspace carve-up (byte offsets)
@@ -102,6 +104,33 @@ struct Model {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   sr_timing timing{};
   bool pdl = true;
+  bool use_tc = true;  // tcgen05 GEMM (K6); SR_GEMM=mma selects the mma.sync reference
+  struct alignas(64) TMap { CUtensorMap m; };
+  std::vector<TMap> wmaps;     // per layer: qkv, o, gu, d ; then lm_head
+  TMap amaps[3][4];            // [x | attn | act][token tile 32/64/128/256]
+  enum { ACT_X = 0, ACT_ATTN = 1, ACT_ACT = 2 };
+
+  int build_tmaps() {
+    wmaps.resize((size_t)d.n_layers * 4 + 1);
+    for (int l = 0; l < d.n_layers; ++l) {
+      const void* w[4] = {lw(l, WQKV), lw(l, WO), lw(l, WGU), lw(l, WD)};
+      const int rows[4] = {qkv_rows, d.d_model, 2 * d.d_ffn, d.d_model};
+      const int cols[4] = {d.d_model, q_dim, d.d_model, d.d_ffn};
+      for (int i = 0; i < 4; ++i)
+        if (make_tmap_bf16(&wmaps[l * 4 + i].m, w[i], rows[i], cols[i], 128))
+          return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for a weight");
+    }
+    if (make_tmap_bf16(&wmaps.back().m, lm_head, d.vocab_rows, d.d_model, 128))
+      return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for lm_head");
+    const void* a[3] = {x, attn, act};
+    const int acols[3] = {d.d_model, q_dim, d.d_ffn};
+    const int tiles[4] = {32, 64, 128, 256};
+    for (int i = 0; i < 3; ++i)
+      for (int t = 0; t < 4; ++t)
+        if (make_tmap_bf16(&amaps[i][t].m, a[i], d.max_tokens, acols[i], tiles[t]))
+          return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for an activation");
+    return 0;
+  }
 
   template <typename T>
   T* at(size_t off) { return reinterpret_cast<T*>(ws + off); }
@@ -247,7 +276,7 @@ struct Model {
       SR_CK(embed_norm_launch(ids + c0, M, embed, d.d_model, lw(0, LN1), d.rms_eps, h, x, s));
       for (int l = 0; l < d.n_layers; ++l) {
         // qkv
-        int rc = gemm(x, lw(l, WQKV), M, qkv_rows, d.d_model, s);
+        int rc = gemm(ACT_X, l * 4 + 0, x, lw(l, WQKV), M, qkv_rows, d.d_model, s);
         if (rc) return -rc;
         EpiParams ep = epi_base(M, qkv_rows);
         ep.bias = lw(l, BQKV);
@@ -275,18 +304,18 @@ struct Model {
         a.st = nullptr;
         SR_CK(attn_prefill_launch(a, M, s));
         // o-proj + residual + norm2
-        rc = gemm(attn, lw(l, WO), M, d.d_model, q_dim, s);
+        rc = gemm(ACT_ATTN, l * 4 + 1, attn, lw(l, WO), M, d.d_model, q_dim, s);
         if (rc) return -rc;
         ep = epi_base(M, d.d_model);
         ep.norm_w = lw(l, LN2);
         SR_CK(epi_resid_norm_launch(ep, s));
         // gate/up
-        rc = gemm(x, lw(l, WGU), M, 2 * d.d_ffn, d.d_model, s);
+        rc = gemm(ACT_X, l * 4 + 2, x, lw(l, WGU), M, 2 * d.d_ffn, d.d_model, s);
         if (rc) return -rc;
         ep = epi_base(M, 2 * d.d_ffn);
         SR_CK(epi_glu_launch(ep, s));
         // down + residual + next norm
-        rc = gemm(act, lw(l, WD), M, d.d_model, d.d_ffn, s);
+        rc = gemm(ACT_ACT, l * 4 + 3, act, lw(l, WD), M, d.d_model, d.d_ffn, s);
         if (rc) return -rc;
         ep = epi_base(M, d.d_model);
         ep.norm_w = (l + 1 < d.n_layers) ? lw(l + 1, LN1) : ln_f;
@@ -298,7 +327,25 @@ struct Model {
   }
 
   int last_splits = 1;
-  int gemm(const __nv_bfloat16* A, const __nv_bfloat16* B, int M, int N, int K, cudaStream_t s) {
+  int gemm(int act_id, int wmap, const __nv_bfloat16* A, const __nv_bfloat16* B, int M, int N,
+           int K, cudaStream_t s) {
+    if (use_tc) {
+      TcGemmArgs a{};
+      const int nt = tc_token_tile(M);
+      const int ti = nt == 32 ? 0 : nt == 64 ? 1 : nt == 128 ? 2 : 3;
+      a.tmW = &wmaps[wmap].m;
+      a.tmX = &amaps[act_id][ti].m;
+      a.C = part;
+      a.M = M;
+      a.N = N;
+      a.K = K;
+      int sp = tc_pick_splits(M, N, K, num_sms);
+      while (sp > 1 && (size_t)sp * M * N > L.part_floats) --sp;
+      a.splits = sp;
+      last_splits = sp;
+      SR_CK(gemm_tc_launch(a, s));
+      return 0;
+    }
     GemmParams g{};
     g.A = A;
     g.B = B;
@@ -418,6 +465,11 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
   }
   for (auto& ev : m->ev) cudaEventCreate(&ev);
   if (const char* v = getenv("SR_NO_PDL")) m->pdl = (v[0] == '0');
+  if (const char* v = getenv("SR_GEMM")) m->use_tc = strcmp(v, "mma") != 0;
+  if (int rc = m->build_tmaps()) {
+    sr_model_destroy(m);
+    return rc;
+  }
   if (int rc = m->build_graph()) {
     sr_model_destroy(m);
     return rc;

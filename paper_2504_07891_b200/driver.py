@@ -257,6 +257,8 @@ class _Run:
         self.rejected: list[ReasoningStep] = []
         self.trace: list[dict] = []
         self.index = 0
+        self.carried = 0.0      # latency of a final no-text end-think, charged to the answer
+        self.exhausted = False  # thinking ended on the budget
 
     def retain(self, text: str, tokens: int, producer: StepProducer,
                score: UtilityScore | None, latency: LatencyBreakdown,
@@ -307,6 +309,52 @@ def run_trajectory(config: EngineConfig, problem: str, small: Backend,
                             trace=run.trace)
 
 
+class SpecReasonSession:
+    """Step-granular SpecReason trajectory (the same loop as
+    ``run_trajectory``): ``step()`` runs one draft -> score -> accept / fall
+    back iteration and returns the retained ``StepOutcome`` (None once
+    thinking has ended); ``finish()`` generates the answer and returns the
+    ``TrajectoryResult``.  Used by the benchmark to time individual steps."""
+
+    def __init__(self, config: EngineConfig, problem: str, small: Backend, base: Backend) -> None:
+        if small.profile.role != BackendRole.SMALL or base.profile.role != BackendRole.BASE:
+            raise ValueError("small/base backends have the wrong roles")
+        self.small, self.base = small, base
+        self.run = _Run(config, problem)
+
+    @property
+    def thinking(self) -> bool:
+        return self.run.state.phase == Phase.THINKING
+
+    def step(self) -> StepOutcome | None:
+        n = len(self.run.outcomes)
+        try:
+            _think_step(self.run, self.small, self.base)
+        except Exception as exc:
+            if not _is_backend_error(exc):
+                raise
+            raise _with_context(exc, self.run.state.problem, len(self.run.state.retained_steps)) from exc
+        return self.run.outcomes[-1] if len(self.run.outcomes) > n else None
+
+    def finish(self) -> TrajectoryResult:
+        run = self.run
+        while self.step() is not None or self.thinking:
+            pass
+        answer_latency = run.carried + _answer(run, self.base)
+        kept = run.state.retained_steps
+        n_spec = sum(1 for s in kept if s.producer == StepProducer.SPECULATOR)
+        metrics = RunMetrics(
+            latency_s=sum(s.latency.total_s for s in kept) + answer_latency,
+            thinking_tokens=run.state.thinking_tokens_used,
+            accepted_fraction=(n_spec / len(kept)) if kept else None,
+            rejected_count=len(run.rejected), correct=False,
+            scheme=Scheme.SPEC_REASON_DECODE if run.config.hierarchical else Scheme.SPEC_REASON,
+            budget_exhausted=run.exhausted)
+        return TrajectoryResult(state=run.state, outcomes=run.outcomes, metrics=metrics,
+                                rejected_steps=run.rejected, answer_latency_s=answer_latency,
+                                trace=run.trace)
+
+
 def _regen_seconds(run: _Run, small: Backend, base: Backend, prompt: str, result) -> float:
     """Fallback cost; simulated + hierarchical runs price token-level rounds."""
     if not base.simulated:
@@ -324,100 +372,104 @@ def _regen_seconds(run: _Run, small: Backend, base: Backend, prompt: str, result
 
 def _think(run: _Run, small: Backend, base: Backend) -> tuple[float, bool]:
     """Thinking phase; returns (latency charged to the answer, budget hit)."""
+    while _think_step(run, small, base):
+        pass
+    return run.carried, run.exhausted
+
+
+def _think_step(run: _Run, small: Backend, base: Backend) -> bool:
+    """One iteration of the thinking loop (engine.py:373-519); False once
+    thinking has ended."""
     config, state = run.config, run.state
+    if state.phase != Phase.THINKING:
+        return False
     problem = state.problem
-    carried = 0.0
-    while state.phase == Phase.THINKING:
-        remaining = state.budget - state.thinking_tokens_used
-        if remaining <= 0:
+    remaining = state.budget - state.thinking_tokens_used
+    if remaining <= 0:
+        run.end_thinking()
+        run.exhausted = True
+        return False
+    cot = state.cot_text()
+    prompt = render_generation_prompt(problem, cot)
+    request = _step_request(prompt, config)
+
+    if force_first_n(config, run.index):
+        res, piece = _generate_piece(base, request, config)
+        secs = _gen_seconds(run.ledger, "base-gen", base, prompt, res)
+        if piece.end_think and not piece.text:
+            run.carried += secs
             run.end_thinking()
-            return carried, True
-        cot = state.cot_text()
-        prompt = render_generation_prompt(problem, cot)
-        request = _step_request(prompt, config)
+            return False
+        text, tokens, hit = _fit_budget(piece, remaining)
+        run.ledger.extend("base-gen", prompt + text)
+        run.retain(text, tokens, StepProducer.BASE_FORCED, None,
+                   LatencyBreakdown(fallback_s=secs), StepAction.FORCED_BASE)
+        return _after_retain(run, hit, piece.end_think)
 
-        if force_first_n(config, run.index):
-            res, piece = _generate_piece(base, request, config)
-            secs = _gen_seconds(run.ledger, "base-gen", base, prompt, res)
-            if piece.end_think and not piece.text:
-                carried += secs
-                run.end_thinking()
-                break
-            text, tokens, hit = _fit_budget(piece, remaining)
-            run.ledger.extend("base-gen", prompt + text)
-            run.retain(text, tokens, StepProducer.BASE_FORCED, None,
-                       LatencyBreakdown(fallback_s=secs), StepAction.FORCED_BASE)
-            if _after_retain(run, hit, piece.end_think):
-                return carried, True
-            continue
+    cand_res, cand = _generate_piece(small, request, config)
+    spec_s = _gen_seconds(run.ledger, "small-gen", small, prompt, cand_res)
 
-        cand_res, cand = _generate_piece(small, request, config)
-        spec_s = _gen_seconds(run.ledger, "small-gen", small, prompt, cand_res)
-
-        if cand.end_think and not cand.text:
-            # the draft proposes to stop thinking: the base confirms or continues
-            conf_res, conf = _generate_piece(base, request, config)
-            conf_s = _gen_seconds(run.ledger, "base-gen", base, prompt, conf_res)
-            if conf.end_think and not conf.text:
-                carried += spec_s + conf_s
-                run.end_thinking()
-                break
-            text, tokens, hit = _fit_budget(conf, remaining)
-            run.ledger.extend("base-gen", prompt + text)
-            run.retain(text, tokens, StepProducer.BASE, None,
-                       LatencyBreakdown(speculate_s=spec_s, fallback_s=conf_s),
-                       StepAction.REJECTED_THEN_REGENERATED)
-            if _after_retain(run, hit, conf.end_think):
-                return carried, True
-            continue
-
-        score, measured = _score(base, VerificationRequest(problem=problem, cot_prefix=cot,
-                                                           candidate_step=cand.text))
-        verify_s = (measured if measured is not None
-                    else _verify_seconds(run.ledger, base, problem, cot, cand.token_count))
-        accepted = score is not None and decide_acceptance(score, config.threshold) == Decision.ACCEPT
-
-        if accepted:
-            text, tokens, hit = _fit_budget(cand, remaining)
-            if small.simulated:
-                run.ledger.extend("small-gen", prompt + text)
-            run.retain(text, tokens, StepProducer.SPECULATOR, score,
-                       LatencyBreakdown(speculate_s=spec_s, verify_s=verify_s),
-                       StepAction.ACCEPTED_SPECULATION)
-            if _after_retain(run, hit, cand.end_think):
-                return carried, True
-            continue
-
-        # Reject: audit copy, then the base regenerates from the same prefix
-        run.rejected.append(ReasoningStep(
-            index=run.index, text=cand.text, token_count=cand.token_count,
-            producer=StepProducer.SPECULATOR, score=score, accepted=False,
-            latency=LatencyBreakdown(speculate_s=spec_s, verify_s=verify_s)))
-        regen_res, regen = _generate_piece(base, request, config)
-        fb_s = _regen_seconds(run, small, base, prompt, regen_res)
-        if regen.end_think and not regen.text:
-            carried += spec_s + verify_s + fb_s
+    if cand.end_think and not cand.text:
+        # the draft proposes to stop thinking: the base confirms or continues
+        conf_res, conf = _generate_piece(base, request, config)
+        conf_s = _gen_seconds(run.ledger, "base-gen", base, prompt, conf_res)
+        if conf.end_think and not conf.text:
+            run.carried += spec_s + conf_s
             run.end_thinking()
-            break
-        text, tokens, hit = _fit_budget(regen, remaining)
+            return False
+        text, tokens, hit = _fit_budget(conf, remaining)
         run.ledger.extend("base-gen", prompt + text)
         run.retain(text, tokens, StepProducer.BASE, None,
-                   LatencyBreakdown(speculate_s=spec_s, verify_s=verify_s, fallback_s=fb_s),
+                   LatencyBreakdown(speculate_s=spec_s, fallback_s=conf_s),
                    StepAction.REJECTED_THEN_REGENERATED)
-        run.trace[-1]["rejected_token_count"] = cand.token_count
-        run.trace[-1]["rejected_score"] = score.value if score is not None else None
-        if _after_retain(run, hit, regen.end_think):
-            return carried, True
-    return carried, False
+        return _after_retain(run, hit, conf.end_think)
+
+    score, measured = _score(base, VerificationRequest(problem=problem, cot_prefix=cot,
+                                                       candidate_step=cand.text))
+    verify_s = (measured if measured is not None
+                else _verify_seconds(run.ledger, base, problem, cot, cand.token_count))
+    accepted = score is not None and decide_acceptance(score, config.threshold) == Decision.ACCEPT
+
+    if accepted:
+        text, tokens, hit = _fit_budget(cand, remaining)
+        if small.simulated:
+            run.ledger.extend("small-gen", prompt + text)
+        run.retain(text, tokens, StepProducer.SPECULATOR, score,
+                   LatencyBreakdown(speculate_s=spec_s, verify_s=verify_s),
+                   StepAction.ACCEPTED_SPECULATION)
+        return _after_retain(run, hit, cand.end_think)
+
+    # Reject: audit copy, then the base regenerates from the same prefix
+    run.rejected.append(ReasoningStep(
+        index=run.index, text=cand.text, token_count=cand.token_count,
+        producer=StepProducer.SPECULATOR, score=score, accepted=False,
+        latency=LatencyBreakdown(speculate_s=spec_s, verify_s=verify_s)))
+    regen_res, regen = _generate_piece(base, request, config)
+    fb_s = _regen_seconds(run, small, base, prompt, regen_res)
+    if regen.end_think and not regen.text:
+        run.carried += spec_s + verify_s + fb_s
+        run.end_thinking()
+        return False
+    text, tokens, hit = _fit_budget(regen, remaining)
+    run.ledger.extend("base-gen", prompt + text)
+    run.retain(text, tokens, StepProducer.BASE, None,
+               LatencyBreakdown(speculate_s=spec_s, verify_s=verify_s, fallback_s=fb_s),
+               StepAction.REJECTED_THEN_REGENERATED)
+    run.trace[-1]["rejected_token_count"] = cand.token_count
+    run.trace[-1]["rejected_score"] = score.value if score is not None else None
+    return _after_retain(run, hit, regen.end_think)
 
 
 def _after_retain(run: _Run, hit_budget: bool, end_think: bool) -> bool:
     """Advance the step index; end thinking on budget or end-think.  Returns
-    True when the budget was hit (the caller reports exhaustion)."""
+    whether thinking continues."""
     run.index += 1
+    if hit_budget:
+        run.exhausted = True
     if hit_budget or end_think:
         run.end_thinking()
-    return hit_budget
+        return False
+    return True
 
 
 def _answer(run: _Run, base: Backend) -> float:
@@ -502,7 +554,8 @@ def _vanilla(config: EngineConfig, problem: str, backend: Backend,
         else:
             lat, action = LatencyBreakdown(fallback_s=secs), StepAction.FORCED_BASE
         run.retain(text, tokens, producer, None, lat, action)
-        exhausted = _after_retain(run, hit, piece.end_think) or exhausted
+        _after_retain(run, hit, piece.end_think)
+        exhausted = exhausted or run.exhausted
 
     state.phase = Phase.ANSWERING
     prompt = render_generation_prompt(problem, state.cot_text(), thinking_done=True)

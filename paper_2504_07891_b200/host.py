@@ -216,7 +216,8 @@ class ModelBackend(Backend):
             if self.record:
                 self.calls.append({"kind": "gen", "prompt_ids": ids, "gen_ids": list(gen),
                                    "finish": finish, "stop": list(request.stop),
-                                   "max_tokens": request.max_tokens})
+                                   "max_tokens": request.max_tokens, "fresh": len(ids) - keep,
+                                   "seq": time.monotonic_ns()})
         T = self.types
         if finish == FINISH_END_THINK:
             text_ids, reason = gen[:-1], T.FinishReason.END_THINK
@@ -244,7 +245,8 @@ class ModelBackend(Backend):
             if self.record:
                 self.calls.append({"kind": "score", "prompt_ids": ids, "score": r.score,
                                    "accept": r.accept, "margin": r.margin,
-                                   "argmax": r.argmax})
+                                   "argmax": r.argmax, "fresh": len(ids) - keep,
+                                   "seq": time.monotonic_ns()})
         if r.score < 0:
             raise T.ScoreParseFailure("no digit in the top-10 or the sampled token")
         return T.UtilityScore(r.score)

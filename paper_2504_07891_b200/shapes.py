@@ -16,12 +16,18 @@ carries a small, documented "judge circuit" in its weights only:
 * the embedding row of the judge-cue word ``"0-9:"`` (the verify template's
   last word, ``prompts.py:66``) is ``cue_gain * sqrt(d) * u`` for a fixed unit
   vector ``u``, so the residual stream at that position points along ``u``;
-* each digit's LM-head row gets ``digit_gain * u / sqrt(d)`` added, lifting
-  all ten digits into the top-10 *only* at the cue position; the random part
-  of those rows (orthogonalised against ``u``) decides which digit wins from
-  the context-dependent remainder of the hidden state.
+* each digit's LM-head row gets ``(digit_gain + judge_offsets[j]) * u / sqrt(d)``
+  added, lifting all ten digits into the top-10 *only* at the cue position;
+  the random part of those rows (orthogonalised against ``u``) decides which
+  digit wins from the context-dependent remainder of the hidden state;
+* ``judge_offsets`` equalise the ten digits' mean logit over synthetic verify
+  prompts (without them the context-independent part of the cue's hidden
+  state pins the score to one or two digits).  They are measured once per
+  (model, seed) by ``tools/calibrate_judge.py`` and stored below; the first
+  padding row of the LM head is a probe ``u / sqrt(d)`` that reads the cue
+  alignment the calibration needs (padding rows are never produced).
 
-Both are plain weight values: the kernels contain no special case for them.
+All of it is plain weight values: the kernels contain no special case.
 """
 
 from __future__ import annotations
@@ -50,11 +56,12 @@ class ModelSpec:
     rope_theta: float = 1_000_000.0
     rms_eps: float = 1e-6
     init_std: float = 0.0    # 0 -> fan-in init N(0, 1/d_in) (see module doc)
-    qk_gain: float = 2.0     # extra scale of the q/k rows: peaked attention
+    qk_gain: float = 1.0     # extra scale of the q/k rows (1 = plain fan-in init)
     judge: bool = False      # install the judge circuit (base models)
     cue_gain: float = 4.0
     digit_gain: float = 6.0
     digit_noise: float = 1.0
+    judge_offsets: tuple = ()  # per-digit gain offsets (tools/calibrate_judge.py)
 
     @property
     def q_dim(self) -> int:
@@ -98,7 +105,8 @@ MODELS: dict[str, ModelSpec] = {
     # C1 tiny pair (SURVEY.md §8 "C1 (proposed)"; head_dim kept at 128 so the
     # tiny pair runs the exact kernels of the full-size models)
     "tiny-draft": ModelSpec("tiny-draft", 2, 128, 2, 1, 512, 4096, 4096, rope_theta=10_000.0),
-    "tiny-base": ModelSpec("tiny-base", 4, 256, 4, 2, 1024, 4096, 4096, judge=True),
+    "tiny-base": ModelSpec("tiny-base", 4, 256, 4, 2, 1024, 4160, 4096, judge=True,
+                           judge_offsets=(-0.5, -0.125, -0.5, 0.375, 0.5, 0.25, 0.0, 0.375, 0.25, -0.5)),
     # public model-card shapes
     "r1-1.5b": ModelSpec("r1-1.5b", 28, 1536, 12, 2, 8960, V_QWEN_DRAFT, V_QWEN_DRAFT,
                          rope_theta=10_000.0),
@@ -198,10 +206,13 @@ def make_tensor(spec: ModelSpec, seed: int, name: str, device: str = "cpu") -> t
         t[JUDGE_CUE_ID] = spec.cue_gain * math.sqrt(spec.d_model) * u
     if spec.judge and name == "lm_head":
         u = _judge_direction(spec, seed).to(device)
+        offs = spec.judge_offsets or (0.0,) * len(DIGIT_IDS)
         for dgt in DIGIT_IDS:
             r = t[dgt] * spec.digit_noise
             r = r - (r @ u) * u
-            t[dgt] = r + (spec.digit_gain / math.sqrt(spec.d_model)) * u
+            t[dgt] = r + ((spec.digit_gain + offs[dgt]) / math.sqrt(spec.d_model)) * u
+        if spec.vocab_rows > spec.vocab_text:
+            t[spec.vocab_text] = u / math.sqrt(spec.d_model)  # cue-alignment probe
     return t.to(torch.bfloat16)
 
 
@@ -225,3 +236,37 @@ def rope_table(spec: ModelSpec, max_pos: int) -> torch.Tensor:
     ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
     tab = np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
     return torch.from_numpy(tab)
+
+
+# --------------------------------------------------------------------------
+# judge calibration (see module doc)
+# --------------------------------------------------------------------------
+
+def judge_calibration_prompts(spec: ModelSpec, n: int = 24) -> list[list[int]]:
+    """Token ids of ``n`` synthetic verify prompts (64-word problem, a CoT of
+    0..600 words, a 24-word candidate), seeded and model-independent."""
+    from .domain import render_verification_prompt
+    from .vocab import shared_vocab
+
+    vocab = shared_vocab(spec.vocab_text)
+    lo, hi = vocab.ordinary_range()
+    rng = np.random.default_rng(20250410)
+    out = []
+    for i in range(n):
+        w = [vocab.words[int(x)] for x in rng.integers(lo, hi, size=64 + 25 * i + 24)]
+        prompt = render_verification_prompt(" ".join(w[:64]), " ".join(w[64:64 + 25 * i]) + " ",
+                                            " ".join(w[64 + 25 * i:]) + " ")
+        out.append(vocab.encode(prompt))
+    return out
+
+
+def judge_offsets_update(spec: ModelSpec, last_logits: list[torch.Tensor]) -> tuple:
+    """One calibration step: new per-digit gain offsets that equalise the
+    digits' mean logit at the cue, from the last-position logits of the
+    calibration prompts (probe row = cue alignment)."""
+    L = torch.stack([x.float().cpu() for x in last_logits])
+    mu = L[:, list(DIGIT_IDS)].mean(0)
+    probe = float(L[:, spec.vocab_text].mean())
+    delta = -(mu - mu.mean()) / probe
+    old = spec.judge_offsets or (0.0,) * len(DIGIT_IDS)
+    return tuple(round((o + float(d)) * 8) / 8 for o, d in zip(old, delta))

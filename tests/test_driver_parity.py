@@ -168,3 +168,16 @@ def test_error_context_and_roles():
     with pytest.raises(contract.TransportError, match="step 2 of problem"):
         driver.run_trajectory(EngineConfig(threshold=AcceptanceThreshold(0)), "p\nmore", small,
                               _Scripted(BackendRole.BASE))
+
+
+def test_session_steps_equal_run_trajectory(stepspec, sim):
+    small, base, tasks = sim
+    cfg = EngineConfig(seed=4, token_budget=120)
+    whole = driver.run_trajectory(cfg, tasks[1].problem_text(), small, base)
+    sess = driver.SpecReasonSession(cfg, tasks[1].problem_text(), small, base)
+    n = 0
+    while sess.step() is not None:
+        n += 1
+    res = sess.finish()
+    assert n == len(res.outcomes)
+    assert _as_plain(res) == _as_plain(whole)

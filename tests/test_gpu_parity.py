@@ -1,0 +1,205 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): per-token logits max-abs <= 2e-2
+(bf16 storage vs the oracle's fp32 arithmetic with the same bf16 storage
+points); greedy tokens, step boundaries, judge scores and accept/reject must be
+identical except where the oracle's own top-2 margin is below that tolerance,
+which is flagged (counted) rather than failed.
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.ref_engine import RefEngine, judge_readout, oracle_backend
+from paper_2504_07891_b200 import AcceptanceThreshold, EngineConfig, run_trajectory, run_vanilla
+from paper_2504_07891_b200.contract import GenerationRequest, VerificationRequest
+from paper_2504_07891_b200.domain import (DEFAULT_STEP_STOP_MARKERS, BackendRole,
+                                          render_generation_prompt)
+from paper_2504_07891_b200.driver import trace_signature, validate_trajectory
+from paper_2504_07891_b200.shapes import get_spec, make_weights
+from paper_2504_07891_b200.vocab import CLASS_END_THINK, CLASS_STOP, shared_vocab
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+GOLDEN = json.loads((Path(__file__).parent / "golden" / "c1_trajectories.json").read_text())
+C1 = GOLDEN["config"]
+
+
+@pytest.fixture(scope="module")
+def tiny(cuda):
+    from paper_2504_07891_b200.backend import B200Backend
+
+    out = {}
+    for name, role in (("tiny-draft", BackendRole.SMALL), ("tiny-base", BackendRole.BASE)):
+        spec = get_spec(name)
+        w = make_weights(spec, 0)
+        out[name] = (B200Backend(spec, role, weights=w, max_ctx=2048, record=True),
+                     RefEngine(spec, w, shared_vocab(spec.vocab_text)))
+    return out
+
+
+def _replay_check(calls, ref: RefEngine, vocab_text: int):
+    """Teacher-force every GPU generation through the oracle; returns
+    (checked, flagged, mismatches)."""
+    checked = flagged = bad = 0
+    for c in calls:
+        if c["kind"] != "gen":
+            continue
+        full = c["prompt_ids"] + c["gen_ids"]
+        lg = ref.logits_teacher_forced(full[:-1])[len(c["prompt_ids"]) - 1:, :vocab_text]
+        for k, t in enumerate(c["gen_ids"]):
+            row = lg[k]
+            top = int(row.argmax())
+            checked += 1
+            if t != top:
+                if float(row[top] - row[t]) < TOL:
+                    flagged += 1
+                else:
+                    bad += 1
+    return checked, flagged, bad
+
+
+@pytest.mark.parametrize("name", ["tiny-draft", "tiny-base"])
+def test_teacher_forced_logits(tiny, name):
+    gpu, ref = tiny[name]
+    v = gpu.vocab
+    ids = v.encode(render_generation_prompt(v.problem(64, 1), "")) * 4  # 264 tokens, 2 chunks
+    s = gpu.pool.streams[0]
+    gpu.engine.truncate(s, 0)
+    got = gpu.engine.forward_logits(s, ids).cpu()[:, : v.n_text]
+    want = ref.logits_teacher_forced(ids)[:, : v.n_text]
+    err = (got - want).abs().max().item()
+    assert err <= TOL, err
+    # incremental prefill (rollback + commit) gives the same logits
+    s2 = gpu.pool.streams[1]
+    gpu.engine.truncate(s2, 0)
+    gpu.engine.forward_logits(s2, ids[:77], all_rows=False)
+    inc = gpu.engine.forward_logits(s2, ids[77:]).cpu()[:, : v.n_text]
+    assert (inc - want[77:]).abs().max().item() <= TOL
+
+
+def test_decode_matches_oracle_replay(tiny):
+    gpu, ref = tiny["tiny-draft"]
+    v = gpu.vocab
+    gpu.calls.clear()
+    for p in range(4):
+        prompt = render_generation_prompt(v.problem(64, 10 + p), "")
+        r = gpu.generate_step(GenerationRequest(prompt=prompt, max_tokens=48, stop=()))
+        assert r.token_count == 48 and r.finish_reason.value == "Length"
+    checked, flagged, bad = _replay_check(gpu.calls, ref, v.n_text)
+    assert checked == 4 * 48 and bad == 0, (checked, flagged, bad)
+    assert flagged <= 0.1 * checked
+
+
+def test_stop_classes_and_end_think(tiny):
+    """Device stop test: a stop-class token ends the step and is kept; an
+    END_THINK-class token ends it and is dropped (http.py:140-143)."""
+    gpu, ref = tiny["tiny-draft"]
+    v = gpu.vocab
+    prompt = render_generation_prompt(v.problem(64, 3), "")
+    free = gpu.generate_step(GenerationRequest(prompt=prompt, max_tokens=12, stop=()))
+    ids = v.encode(free.text)
+    # make the 5th generated word a stop string
+    stop_word = v.render_one(ids[4])
+    r = gpu.generate_step(GenerationRequest(prompt=prompt, max_tokens=12, stop=(stop_word,)))
+    assert v.encode(r.text) == ids[: ids.index(ids[4]) + 1] and r.finish_reason.value == "Stop"
+    # max_tokens = 1
+    r1 = gpu.generate_step(GenerationRequest(prompt=prompt, max_tokens=1, stop=()))
+    assert v.encode(r1.text) == ids[:1] and r1.finish_reason.value == "Length"
+    # END_THINK class on the 3rd token via a patched class table
+    eng = gpu.engine
+    key = ("__test_end_think__",)
+    cls = eng._class_table(()).clone()
+    cls[ids[2]] = CLASS_END_THINK
+    eng._classes[key] = cls
+    k = ids.index(ids[2])
+    r2 = gpu.generate_step(GenerationRequest(prompt=prompt, max_tokens=12, stop=key))
+    assert r2.finish_reason.value == "EndThink" and v.encode(r2.text) == ids[:k]
+
+
+def test_judge_readout_matches_oracle(tiny):
+    gpu, ref = tiny["tiny-base"]
+    v = gpu.vocab
+    rng = np.random.default_rng(0)
+    agree = flagged = 0
+    for i in range(24):
+        words = [v.words[int(x)] for x in rng.integers(16, v.n_text, size=160)]
+        req = VerificationRequest(" ".join(words[:64]), " ".join(words[64:136]) + " ",
+                                  " ".join(words[136:]) + " ")
+        gpu.calls.clear()
+        try:
+            got = gpu.score_step(req).value
+        except Exception as exc:  # parse failure
+            assert type(exc).__name__ == "ScoreParseFailure"
+            got = -1
+        ids = gpu.calls[-1]["prompt_ids"]
+        cache = ref.model.new_cache()
+        logits = ref.model.forward(cache, ids)
+        want = judge_readout(logits, v, 7)
+        if got == want.score:
+            agree += 1
+        else:
+            assert want.margin < TOL, (got, want)
+            flagged += 1
+        assert gpu.calls[-1]["accept"] == (got >= 7)
+    assert agree >= 22
+
+
+def test_tiny_trajectories_match_golden_or_flag(tiny):
+    """C1 on the GPU: identical to the golden trajectory produced by the
+    reference engine + oracle, unless a flagged near-tie diverged it; every
+    GPU generation is then replay-checked against the oracle."""
+    from paper_2504_07891_b200.backend import build_pair
+
+    small, base = build_pair("tiny", max_ctx=2048, record=True)
+    v = shared_vocab(4096)
+    identical = 0
+    cases = [c for c in GOLDEN["cases"] if c["kind"] == "spec_reason"]
+    for case in cases:
+        base.threshold = case["threshold"]
+        cfg = EngineConfig(threshold=AcceptanceThreshold(case["threshold"]), **C1)
+        res = run_trajectory(cfg, v.problem(64, case["problem_seed"]), small, base)
+        validate_trajectory(res, cfg)
+        identical += json.loads(json.dumps(trace_signature(res))) == case["signature"]
+    ds = _replay_check(small.calls, tiny["tiny-draft"][1], v.n_text)
+    bs = _replay_check(base.calls, tiny["tiny-base"][1], v.n_text)
+    assert ds[2] == 0 and bs[2] == 0, (ds, bs)
+    assert identical >= len(cases) - 2, identical
+
+
+def test_forced_reject_equals_pure_base_on_gpu(cuda):
+    """Acceptance criterion C1 (test_acceptance.py:104-113) on the device."""
+    from paper_2504_07891_b200.backend import build_pair
+
+    small, base = build_pair("tiny", max_ctx=2048, threshold=10)
+    v = shared_vocab(4096)
+    cfg = EngineConfig(threshold=AcceptanceThreshold(10), **C1)
+    for p in range(2):
+        spec = run_trajectory(cfg, v.problem(64, p), small, base)
+        pure = run_vanilla(cfg, v.problem(64, p), base)
+        assert spec.state.cot_text() == pure.state.cot_text()
+        assert spec.state.final_answer == pure.state.final_answer
+    cfg0 = EngineConfig(threshold=AcceptanceThreshold(0), **C1)
+    base.threshold = 0
+    res = run_trajectory(cfg0, v.problem(64, 0), small, base)
+    assert all(s.producer.value == "Speculator" for s in res.state.retained_steps)
+
+
+def test_deterministic_and_rollback_idempotent(tiny):
+    gpu, _ = tiny["tiny-draft"]
+    v = gpu.vocab
+    prompt = render_generation_prompt(v.problem(64, 7), "")
+    req = GenerationRequest(prompt=prompt, max_tokens=40, stop=DEFAULT_STEP_STOP_MARKERS)
+    a = gpu.generate_step(req).text
+    # continue past it, then come back: the stream rolls back to the prompt
+    gpu.generate_step(GenerationRequest(prompt=prompt + a, max_tokens=40, stop=()))
+    b = gpu.generate_step(req).text
+    for s in gpu.pool.streams:  # cold streams
+        gpu.engine.truncate(s, 0)
+    c = gpu.generate_step(req).text
+    assert a == b == c

@@ -1,0 +1,57 @@
+"""Measure the judge-circuit offsets of a base model (see shapes.py).
+
+    python tools/calibrate_judge.py tiny-base            # CPU oracle (tiny shapes)
+    python tools/calibrate_judge.py qwen2.5-7b --gpu      # on the B200 (full shapes)
+
+Prints the offsets to paste into shapes.MODELS and the score histogram over
+the calibration prompts before/after."""
+
+from __future__ import annotations
+
+import collections
+import dataclasses
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_2504_07891_b200.shapes import (get_spec, judge_calibration_prompts,  # noqa: E402
+                                          judge_offsets_update, make_weights)
+
+
+def logits_fn_for(spec, gpu: bool):
+    w = make_weights(spec, 0, device="cuda" if gpu else "cpu")
+    if gpu:
+        from paper_2504_07891_b200.backend import B200Backend
+        from paper_2504_07891_b200.domain import BackendRole
+
+        b = B200Backend(spec, BackendRole.BASE, weights=w, max_ctx=2048)
+        s = b.pool.streams[0]
+
+        def fn(ids):
+            b.engine.truncate(s, 0)
+            return b.engine.forward_logits(s, ids, all_rows=False)[0].cpu()
+        return fn
+    from oracle.ref_model import RefModel
+
+    m = RefModel(spec, w)
+    return lambda ids: m.forward(m.new_cache(), ids)
+
+
+def main() -> None:
+    name = sys.argv[1]
+    gpu = "--gpu" in sys.argv
+    spec = get_spec(name)
+    prompts = judge_calibration_prompts(spec)
+    for it in range(3):
+        fn = logits_fn_for(spec, gpu)
+        rows = [fn(p) for p in prompts]
+        hist = collections.Counter(int(r[:10].argmax()) for r in rows)
+        print(f"iter {it}: offsets {spec.judge_offsets} -> argmax-digit histogram {sorted(hist.items())}",
+              flush=True)
+        spec = dataclasses.replace(spec, judge_offsets=judge_offsets_update(spec, rows))
+    print("judge_offsets =", spec.judge_offsets)
+
+
+if __name__ == "__main__":
+    main()
