@@ -417,6 +417,10 @@ def run_reference(args) -> None:
 
 
 def main() -> None:
+    if os.environ.get("BENCH_STACK_DUMP_S"):
+        import faulthandler
+
+        faulthandler.dump_traceback_later(int(os.environ["BENCH_STACK_DUMP_S"]), repeat=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)

@@ -34,7 +34,7 @@ from paper_2504_07891_b200.shapes import ModelSpec, gu_split, rope_table
 
 
 def _r(x: torch.Tensor, on: bool) -> torch.Tensor:
-    return x.to(torch.bfloat16).to(torch.float32) if on else x
+    return x.to(torch.bfloat16).to(x.dtype) if on else x
 
 
 class RefModel:
@@ -42,10 +42,14 @@ class RefModel:
 
     def __init__(self, spec: ModelSpec, weights: dict[str, torch.Tensor],
                  max_pos: int = 32768, exact_fp32: bool = False,
-                 layers: list[int] | None = None) -> None:
+                 layers: list[int] | None = None, dtype: torch.dtype = torch.float32) -> None:
+        """``dtype=torch.float64`` keeps the same bf16 storage points but
+        computes in double: the pair (fp32, fp64) measures the intrinsic
+        summation-order noise floor any fp32 implementation has."""
         self.spec = spec
         self.round = not exact_fp32
-        f = lambda t: t.to(torch.float32).contiguous()  # noqa: E731
+        self.dtype = dtype
+        f = lambda t: t.to(dtype).contiguous()  # noqa: E731
         self.embed = f(weights["embed"])
         self.ln_f = f(weights["ln_f"])
         self.lm_head = f(weights["lm_head"])
@@ -60,7 +64,7 @@ class RefModel:
                 "ln2": f(weights[p + "ln2"]), "wg": f(gate), "wu": f(up),
                 "wd": f(weights[p + "wd"]),
             })
-        tab = rope_table(spec, max_pos)
+        tab = rope_table(spec, max_pos).to(dtype)
         self.cos, self.sin = tab[..., 0], tab[..., 1]
 
     # -- cache -----------------------------------------------------------

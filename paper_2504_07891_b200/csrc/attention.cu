@@ -19,6 +19,8 @@ namespace sr {
 constexpr int kAttnThreads = 128;
 constexpr int kStreams = kAttnThreads / 16;
 constexpr int kMaxGroup = 8;
+constexpr int kMaxSplit = 64;    // grid.y <= kMaxSplit
+constexpr int kMinChunk = 64;    // positions per split at least (one page)
 
 template <int G>
 __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnParams p) {
@@ -37,7 +39,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnParams p) {
   const int* ptab = decode ? p.st->page_table : p.page_table;
   const int nsplit = p.nsplit;
   int chunk = (T + nsplit - 1) / nsplit;
-  chunk = chunk < 16 ? 16 : chunk;
+  chunk = chunk < kMinChunk ? kMinChunk : ((chunk + 15) & ~15);
   const int lo = split * chunk;
   const int hi = min(T, lo + chunk);
 
@@ -143,22 +145,43 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnParams p) {
   if (!s_last) return;
   __threadfence();
 
-  // ---- last CTA of (g, m): merge the splits ----
+  // ---- last CTA of (g, m): merge the splits (parallel over splits) ----
+  // 1) split weights w_s = exp2(m_s - M) / L into shared memory
+  float* wsm = &s_acc[0][0][0];         // reuse: G * kMaxSplit split maxima -> weights
+  float* lsm = wsm + G * kMaxSplit;     //        G * kMaxSplit split sums
+  for (int idx = tid; idx < G * nsplit; idx += kAttnThreads) {
+    const int j = idx / nsplit, sp = idx % nsplit;
+    const float* ps = p.part + (((size_t)m * p.n_heads + g * G + j) * nsplit + sp) * part_stride;
+    wsm[j * kMaxSplit + sp] = __ldcg(ps + kHeadDim);
+    lsm[j * kMaxSplit + sp] = __ldcg(ps + kHeadDim + 1);
+  }
+  __syncthreads();
+  if (tid < G) {
+    const int j = tid;
+    float M = -INFINITY;
+    for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, wsm[j * kMaxSplit + sp]);
+    float L = 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float ms = wsm[j * kMaxSplit + sp];
+      const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      L += w * lsm[j * kMaxSplit + sp];
+      wsm[j * kMaxSplit + sp] = w;
+    }
+    const float inv = 1.f / L;
+    for (int sp = 0; sp < nsplit; ++sp) wsm[j * kMaxSplit + sp] *= inv;
+  }
+  __syncthreads();
+  // 2) out[j][d] = sum_s w_s * acc_s[d]; independent loads, unrolled
   for (int idx = tid; idx < G * kHeadDim; idx += kAttnThreads) {
     const int j = idx / kHeadDim, d = idx % kHeadDim;
-    const float* base = p.part + (((size_t)m * p.n_heads + g * G + j) * nsplit) * part_stride;
-    float M = -INFINITY;
-    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(base + s * part_stride + kHeadDim));
-    float L = 0.f, A = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float* ps = base + s * part_stride;
-      const float ms = __ldcg(ps + kHeadDim);
-      if (ms == -INFINITY) continue;
-      const float w = exp2f(ms - M);
-      L += __ldcg(ps + kHeadDim + 1) * w;
-      A += __ldcg(ps + d) * w;
+    const float* base = p.part + (((size_t)m * p.n_heads + g * G + j) * nsplit) * part_stride + d;
+    float A = 0.f;
+#pragma unroll 8
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float w = wsm[j * kMaxSplit + sp];
+      if (w != 0.f) A = fmaf(w, __ldcg(base + sp * part_stride), A);
     }
-    p.out[(size_t)m * qdim + (size_t)(g * G + j) * kHeadDim + d] = __float2bfloat16_rn(A / L);
+    p.out[(size_t)m * qdim + (size_t)(g * G + j) * kHeadDim + d] = __float2bfloat16_rn(A);
   }
   (void)n_rows;
 }
@@ -191,11 +214,23 @@ static cudaError_t launch_any(const AttnParams& p, int M, cudaStream_t stream, b
   return cudaErrorInvalidValue;
 }
 
+int attn_decode_splits(int n_kv, int num_sms) {
+  int s = (num_sms + n_kv - 1) / n_kv;  // ~one CTA per SM at long contexts
+  return s < 1 ? 1 : (s > kMaxSplit ? kMaxSplit : s);
+}
+
+int attn_prefill_splits(int T) {
+  const int s = (T + 511) / 512;
+  return s < 1 ? 1 : (s > 16 ? 16 : s);
+}
+
 cudaError_t attn_decode_launch(const AttnParams& p, cudaStream_t stream, bool pdl) {
+  if (p.nsplit > kMaxSplit) return cudaErrorInvalidValue;
   return launch_any(p, 1, stream, pdl);
 }
 
 cudaError_t attn_prefill_launch(const AttnParams& p, int M, cudaStream_t stream) {
+  if (p.nsplit > kMaxSplit) return cudaErrorInvalidValue;
   return launch_any(p, M, stream, false);
 }
 

@@ -1,0 +1,566 @@
+// K4 / K7: paged GQA flash attention on the tensor cores (mma.sync m16n8k16,
+// bf16 in, fp32 accumulate), one kernel for decode and prefill.
+//
+// Query rows are (token, head-in-group) pairs of one KV head: row r = token
+// r / G, head g*G + r % G, so the G heads sharing a KV head form the MMA's M
+// dimension and every K/V byte is read once per 64-row query tile.
+//
+// CTA = (kv head, KV split, 64-row query tile); 4 warps.  K and V tiles are
+// one page (64 positions x 128 dims bf16 = 16 KB each, contiguous in the page
+// pool) staged by cp.async into a 2-deep ring with a 16-byte-chunk XOR
+// swizzle so ldmatrix is conflict-free.  Each warp owns 16 query rows and
+// runs S = Q K^T (8 n-tiles x 8 k-steps), an exp2 online softmax in
+// registers, P (re-packed to bf16 A fragments, FA2-style) and O += P V
+// (ldmatrix.trans on V).
+//   decode  (M rows <= 16): the 4 warps split the KV tiles of the CTA among
+//           themselves and merge (m, l, O) through shared memory;
+//   prefill (M rows > 16): the 4 warps own 4 row tiles and share KV tiles;
+//           causality: row r sees positions <= start_pos + r / G.
+// With several KV splits per (kv head, query tile) each CTA writes a partial
+// (m, l, O) and the last CTA (atomic ticket) merges them.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sr {
+
+constexpr int kTcaThreads = 128;
+constexpr int kRowsPerCta = 64;
+constexpr int kTile = kPage;                // 64 positions per KV tile
+constexpr int kTileBytes = kTile * kHeadDim * 2;  // 16 KB
+constexpr int kAttnMaxSplit = 64;
+constexpr float kScaleLog2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
+
+SR_DEV uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+SR_DEV void cpa16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+}
+SR_DEV void cpa_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+SR_DEV void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// swizzled byte offset of (row, 16B-chunk) in a [64][128] bf16 tile
+SR_DEV uint32_t swz(int row, int chunk) { return row * 256 + ((chunk ^ (row & 7)) << 4); }
+
+SR_DEV void ldsm4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+SR_DEV void ldsm4t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+SR_DEV void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                     uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+struct TcaSmem {
+  __align__(128) uint8_t k[2][kTileBytes];
+  __align__(128) uint8_t v[2][kTileBytes];
+  __align__(128) uint8_t q[kRowsPerCta * kHeadDim * 2];
+};
+
+// Per-warp flash state for 16 query rows (thread holds rows g and g+8).
+struct Flash {
+  float o[16][4];   // 16 dim n-tiles x {row g: c0,c1 ; row g+8: c2,c3}
+  float m[2], l[2];
+};
+
+template <bool CAUSAL>
+SR_DEV void flash_tile(Flash& F, const uint32_t (&qa)[8][4], uint32_t ks, uint32_t vs, int lane,
+                       int tile_pos0, int lim0, int lim1) {
+  // S = Q K^T for 16 rows x 64 positions
+  float s[8][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {      // 16-dim k-steps
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {    // pairs of 8-position n-tiles
+      // x4: (pos 0-7, dims kk*16+0..7), (pos 0-7, +8..15), (pos 8-15, +0..7), (pos 8-15, +8..15)
+      const int row = np * 16 + ((lane >> 4) << 3) + (lane & 7);
+      const int chunk = kk * 2 + ((lane >> 3) & 1);
+      uint32_t b[4];
+      ldsm4(b, ks + swz(row, chunk));
+      mma_bf16(s[2 * np], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[0], b[1]);
+      mma_bf16(s[2 * np + 1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[2], b[3]);
+    }
+  }
+  // scale to log2 units in fp32 (q stays exactly the stored bf16), mask,
+  // online softmax
+  const int t = lane & 3;
+  float mx0 = F.m[0], mx1 = F.m[1];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[n][e] *= kScaleLog2;
+    const int p0 = tile_pos0 + n * 8 + 2 * t;
+    if (CAUSAL) {
+      if (p0 > lim0) s[n][0] = -INFINITY;
+      if (p0 + 1 > lim0) s[n][1] = -INFINITY;
+      if (p0 > lim1) s[n][2] = -INFINITY;
+      if (p0 + 1 > lim1) s[n][3] = -INFINITY;
+    }
+    mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
+    mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
+  }
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+  const float base0 = mx0 == -INFINITY ? 0.f : mx0;
+  const float base1 = mx1 == -INFINITY ? 0.f : mx1;
+  const float c0 = exp2f(F.m[0] - base0), c1 = exp2f(F.m[1] - base1);
+  F.m[0] = mx0;
+  F.m[1] = mx1;
+  float rs0 = 0.f, rs1 = 0.f;
+  // P as bf16 A fragments for 4 position k-steps of 16, split hi + lo so the
+  // P V product keeps ~16 mantissa bits of P (the oracle keeps P in fp32)
+  uint32_t pa[4][4], pl[4][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    const float e0 = exp2f(s[n][0] - base0), e1 = exp2f(s[n][1] - base0);
+    const float e2 = exp2f(s[n][2] - base1), e3 = exp2f(s[n][3] - base1);
+    rs0 += e0 + e1;
+    rs1 += e2 + e3;
+    const uint32_t h01 = f2_to_bf2(e0, e1), h23 = f2_to_bf2(e2, e3);
+    const float2 r01 = bf2_to_f2(h01), r23 = bf2_to_f2(h23);
+    const uint32_t l01 = f2_to_bf2(e0 - r01.x, e1 - r01.y), l23 = f2_to_bf2(e2 - r23.x, e3 - r23.y);
+    const int kk = n >> 1, o = (n & 1) * 2;
+    pa[kk][o] = h01;
+    pa[kk][o + 1] = h23;
+    pl[kk][o] = l01;
+    pl[kk][o + 1] = l23;
+  }
+  F.l[0] = F.l[0] * c0 + rs0;
+  F.l[1] = F.l[1] * c1 + rs1;
+#pragma unroll
+  for (int d = 0; d < 16; ++d) {
+    F.o[d][0] *= c0; F.o[d][1] *= c0;
+    F.o[d][2] *= c1; F.o[d][3] *= c1;
+  }
+  // O += P V : k = positions (4 steps of 16), n = dims (16 tiles of 8)
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+    for (int dp = 0; dp < 8; ++dp) {  // pairs of dim n-tiles
+      // trans x4: (pos kk*16+0..7, dims dp*16+0..7), (pos +8..15, same dims),
+      //           (pos +0..7, dims +8..15), (pos +8..15, dims +8..15)
+      const int row = kk * 16 + (((lane >> 3) & 1) << 3) + (lane & 7);
+      const int chunk = dp * 2 + (lane >> 4);
+      uint32_t b[4];
+      ldsm4t(b, vs + swz(row, chunk));
+      mma_bf16(F.o[2 * dp], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b[0], b[1]);
+      mma_bf16(F.o[2 * dp + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b[2], b[3]);
+      mma_bf16(F.o[2 * dp], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b[0], b[1]);
+      mma_bf16(F.o[2 * dp + 1], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b[2], b[3]);
+    }
+  }
+}
+
+// Query row -> (token, head) inside one kv head's group
+SR_DEV const __nv_bfloat16* q_row_ptr(const AttnParams& p, int G, int g, int r) {
+  const int tok = r / G, j = r % G;
+  return p.q + (size_t)tok * p.n_heads * kHeadDim + (size_t)(g * G + j) * kHeadDim;
+}
+
+__global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams p, int M_rows, int G) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  TcaSmem& sm = *reinterpret_cast<TcaSmem*>(smem_raw);
+  __shared__ bool s_last;
+
+  grid_launch_dependents();
+  grid_wait();
+
+  const int g = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int* ptab = p.page_table;
+  const int start = p.start_pos;  // position of token 0
+  const int row0 = qt * kRowsPerCta;
+  const int rows_here = min(kRowsPerCta, M_rows - row0);
+  constexpr bool warp_split_kv = false;  // (decode has its own cluster kernel)
+
+  // KV extent of this query tile: positions <= start + last token of the tile
+  const int last_tok = (row0 + rows_here - 1) / G;
+  const int T = start + last_tok + 1;
+  const int n_tiles = (T + kTile - 1) / kTile;
+  const int nsplit = gridDim.y;
+  const int per = (n_tiles + nsplit - 1) / nsplit;
+  const int t_lo = split * per;
+  const int t_hi = min(n_tiles, t_lo + per);
+
+  // ---- Q tile -> smem (bf16 as stored), swizzled rows ----
+  const uint32_t qs = s_u32(sm.q);
+  for (int i = tid; i < kRowsPerCta * 16; i += kTcaThreads) {
+    const int r = i >> 4, c = i & 15;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < rows_here) {
+      v = reinterpret_cast<const uint4*>(q_row_ptr(p, G, g, row0 + r))[c];
+    }
+    *reinterpret_cast<uint4*>(sm.q + swz(r, c)) = v;
+  }
+
+  // ---- KV tile loader (one page: 64 rows x 256 B for K and for V) ----
+  auto load_tile = [&](int tile, int buf) {
+    const int page = ptab[tile];
+    const size_t off = kv_offset(p.layer, page, g, 0, p.n_pages, p.n_kv);
+    const uint8_t* kg = reinterpret_cast<const uint8_t*>(p.k_pool + off);
+    const uint8_t* vg = reinterpret_cast<const uint8_t*>(p.v_pool + off);
+    const uint32_t kb = s_u32(sm.k[buf]), vb = s_u32(sm.v[buf]);
+    for (int i = tid; i < kTile * 16; i += kTcaThreads) {
+      const int r = i >> 4, c = i & 15;
+      cpa16(kb + swz(r, c), kg + r * 256 + c * 16);
+      cpa16(vb + swz(r, c), vg + r * 256 + c * 16);
+    }
+  };
+
+  // which tiles this warp consumes, and which query rows it owns
+  const int my_rows0 = warp * 16;
+  Flash F;
+#pragma unroll
+  for (int d = 0; d < 16; ++d) F.o[d][0] = F.o[d][1] = F.o[d][2] = F.o[d][3] = 0.f;
+  F.m[0] = F.m[1] = -INFINITY;
+  F.l[0] = F.l[1] = 0.f;
+  const int gq = lane >> 2;
+  const int r_a = row0 + my_rows0 + gq, r_b = r_a + 8;
+  const int lim_a = start + (r_a < M_rows ? r_a : M_rows - 1) / G;
+  const int lim_b = start + (r_b < M_rows ? r_b : M_rows - 1) / G;
+
+  if (t_lo < t_hi) load_tile(t_lo, 0);
+  cpa_commit();
+  __syncthreads();  // Q tile visible
+
+  uint32_t qa[8][4];
+  const bool warp_active = my_rows0 < rows_here;
+  if (warp_active) {
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int row = my_rows0 + (lane & 15);
+      const int chunk = kk * 2 + (lane >> 4);
+      ldsm4(qa[kk], qs + swz(row, chunk));
+    }
+  }
+
+  for (int tile = t_lo; tile < t_hi; ++tile) {
+    const int buf = (tile - t_lo) & 1;
+    if (tile + 1 < t_hi) load_tile(tile + 1, buf ^ 1);
+    cpa_commit();
+    cpa_wait<1>();
+    __syncthreads();
+    if (warp_active) {
+      const int pos0 = tile * kTile;
+      // warp-uniform (the tile functions are full of .sync.aligned ops): mask
+      // whenever the tile reaches past the warp's *first* row's limit
+      const int warp_lim = start + (row0 + my_rows0) / G;
+      const bool need_mask = pos0 + kTile - 1 > warp_lim;
+      const uint32_t ks = s_u32(sm.k[buf]), vs = s_u32(sm.v[buf]);
+      if (need_mask) flash_tile<true>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
+      else flash_tile<false>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
+    }
+    __syncthreads();
+  }
+  cpa_wait<0>();
+
+  // ---- finalise row sums within the quad ----
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    F.l[i] += __shfl_xor_sync(0xffffffffu, F.l[i], 1);
+    F.l[i] += __shfl_xor_sync(0xffffffffu, F.l[i], 2);
+  }
+
+  const size_t part_stride = kHeadDim + 2;
+  {
+    // prefill: each warp writes its own 16 rows straight from registers
+    if (warp_active) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = my_rows0 + gq + 8 * h;
+        if (rr >= rows_here) continue;
+        const int r = row0 + rr;
+        const float Lx = F.l[h], Mx = F.m[h];
+        if (nsplit == 1) {
+          __nv_bfloat16* o = const_cast<__nv_bfloat16*>(q_row_ptr(p, G, g, r)) - p.q + p.out;
+          const float inv = Lx > 0.f ? 1.f / Lx : 0.f;
+          for (int d = 0; d < 16; ++d) {
+            const int col = d * 8 + 2 * (lane & 3);
+            *reinterpret_cast<uint32_t*>(o + col) = f2_to_bf2(F.o[d][2 * h] * inv, F.o[d][2 * h + 1] * inv);
+          }
+        } else {
+          float* part = p.part + ((size_t)r * nsplit + split) * part_stride + (size_t)g * M_rows * nsplit * part_stride;
+          for (int d = 0; d < 16; ++d) {
+            const int col = d * 8 + 2 * (lane & 3);
+            part[col] = F.o[d][2 * h];
+            part[col + 1] = F.o[d][2 * h + 1];
+          }
+          if ((lane & 3) == 0) { part[kHeadDim] = Mx; part[kHeadDim + 1] = Lx; }
+        }
+      }
+    }
+  }
+  if (nsplit == 1) return;
+
+  // ---- split merge: last CTA of (kv head, query tile) ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned int* ctr = p.counters + (size_t)qt * p.n_kv + g;
+    const unsigned prev = atomicAdd(ctr, 1u);
+    s_last = (prev == (unsigned)nsplit - 1);
+    if (s_last) *ctr = 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  float* wsm = reinterpret_cast<float*>(sm.v[0]);  // [64 rows][kAttnMaxSplit] weights
+  for (int idx = tid; idx < rows_here * nsplit; idx += kTcaThreads) {
+    const int rr = idx / nsplit, sp = idx % nsplit;
+    const float* ps = p.part + ((size_t)(row0 + rr) * nsplit + sp) * part_stride +
+                      (size_t)g * M_rows * nsplit * part_stride;
+    wsm[rr * kAttnMaxSplit + sp] = __ldcg(ps + kHeadDim);
+    wsm[(kRowsPerCta + rr) * kAttnMaxSplit + sp] = __ldcg(ps + kHeadDim + 1);
+  }
+  __syncthreads();
+  for (int rr = tid; rr < rows_here; rr += kTcaThreads) {
+    float M = -INFINITY;
+    for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, wsm[rr * kAttnMaxSplit + sp]);
+    float L = 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float ms = wsm[rr * kAttnMaxSplit + sp];
+      const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      L += w * wsm[(kRowsPerCta + rr) * kAttnMaxSplit + sp];
+      wsm[rr * kAttnMaxSplit + sp] = w;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) wsm[rr * kAttnMaxSplit + sp] *= inv;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < rows_here * kHeadDim; idx += kTcaThreads) {
+    const int rr = idx / kHeadDim, d = idx % kHeadDim;
+    const float* base = p.part + ((size_t)(row0 + rr) * nsplit) * part_stride +
+                        (size_t)g * M_rows * nsplit * part_stride + d;
+    float A = 0.f;
+#pragma unroll 8
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float w = wsm[rr * kAttnMaxSplit + sp];
+      if (w != 0.f) A = fmaf(w, __ldcg(base + (size_t)sp * part_stride), A);
+    }
+    __nv_bfloat16* o = const_cast<__nv_bfloat16*>(q_row_ptr(p, G, g, row0 + rr)) - p.q + p.out;
+    o[d] = __float2bfloat16_rn(A);
+  }
+}
+
+// ----------------------------------------------------------------- decode --
+// One cluster of kDecCluster CTAs per KV head; the G query heads of the group
+// are the 16-row M tile.  KV tile i (64 positions) belongs to CTA i % C and,
+// inside it, to warp (i / C) % 4; each warp streams its tiles through a
+// private single-buffered K/V slot.  Warps merge (m, l, O) in shared memory,
+// then CTA rank 0 merges the cluster over DSMEM -- no global partials, no
+// atomics, no second kernel.
+constexpr int kDecCluster = 8;
+constexpr int kDecWarps = 4;
+
+struct DecSmem {
+  __align__(128) uint8_t kv[kDecWarps][2][kTileBytes];  // per-warp K, V
+  __align__(128) uint8_t q[16 * kHeadDim * 2];
+  float o[16][kHeadDim];        // CTA-merged, unnormalised O (rescaled to m)
+  float m[16], l[16];
+  float wm[kDecWarps][16], wl[kDecWarps][16];
+};
+
+__global__ void __cluster_dims__(1, kDecCluster, 1) __launch_bounds__(kDecWarps * 32)
+    attn_decode_tc_kernel(AttnParams p, int G) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  DecSmem& sm = *reinterpret_cast<DecSmem*>(smem_raw);
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+
+  grid_launch_dependents();
+  grid_wait();
+  const bool done = p.st->done != 0;  // uniform across the cluster
+
+  const int g = blockIdx.x;
+  const int crank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2;
+
+  Flash F;
+#pragma unroll
+  for (int d = 0; d < 16; ++d) F.o[d][0] = F.o[d][1] = F.o[d][2] = F.o[d][3] = 0.f;
+  F.m[0] = F.m[1] = -INFINITY;
+  F.l[0] = F.l[1] = 0.f;
+
+  if (!done) {
+    const int T = p.st->ctx_len;
+    const int* ptab = p.st->page_table;
+    const int n_tiles = (T + kTile - 1) / kTile;
+    // Q (G rows) -> smem, rows >= G zero
+    const uint32_t qs = s_u32(sm.q);
+    for (int i = tid; i < 16 * 16; i += kDecWarps * 32) {
+      const int r = i >> 4, c = i & 15;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < G) {
+        v = reinterpret_cast<const uint4*>(p.q + (size_t)(g * G + r) * kHeadDim)[c];
+      }
+      *reinterpret_cast<uint4*>(sm.q + swz(r, c)) = v;
+    }
+    __syncthreads();
+    uint32_t qa[8][4];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) ldsm4(qa[kk], qs + swz(lane & 15, kk * 2 + (lane >> 4)));
+
+    const uint32_t ks = s_u32(sm.kv[warp][0]), vs = s_u32(sm.kv[warp][1]);
+    const int lim = T - 1;
+    for (int i = crank + kDecCluster * warp; i < n_tiles; i += kDecCluster * kDecWarps) {
+      const int page = ptab[i];
+      const size_t off = kv_offset(p.layer, page, g, 0, p.n_pages, p.n_kv);
+      const uint8_t* kg = reinterpret_cast<const uint8_t*>(p.k_pool + off);
+      const uint8_t* vg = reinterpret_cast<const uint8_t*>(p.v_pool + off);
+#pragma unroll 4
+      for (int j = lane; j < kTile * 16; j += 32) {
+        const int r = j >> 4, c = j & 15;
+        cpa16(ks + swz(r, c), kg + r * 256 + c * 16);
+        cpa16(vs + swz(r, c), vg + r * 256 + c * 16);
+      }
+      cpa_commit();
+      cpa_wait<0>();
+      __syncwarp();
+      const int pos0 = i * kTile;
+      if (pos0 + kTile - 1 > lim) flash_tile<true>(F, qa, ks, vs, lane, pos0, lim, lim);
+      else flash_tile<false>(F, qa, ks, vs, lane, pos0, lim, lim);
+      __syncwarp();
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      F.l[h] += __shfl_xor_sync(0xffffffffu, F.l[h], 1);
+      F.l[h] += __shfl_xor_sync(0xffffffffu, F.l[h], 2);
+    }
+  }
+
+  // ---- merge the 4 warps of this CTA ----
+  if ((lane & 3) == 0) {
+    sm.wm[warp][gq] = F.m[0];
+    sm.wm[warp][gq + 8] = F.m[1];
+    sm.wl[warp][gq] = F.l[0];
+    sm.wl[warp][gq + 8] = F.l[1];
+  }
+  for (int i = tid; i < 16 * kHeadDim; i += kDecWarps * 32) (&sm.o[0][0])[i] = 0.f;
+  __syncthreads();
+  if (tid < 16) {
+    float M = -INFINITY, L = 0.f;
+    for (int w = 0; w < kDecWarps; ++w) M = fmaxf(M, sm.wm[w][tid]);
+    for (int w = 0; w < kDecWarps; ++w) {
+      const float mw = sm.wm[w][tid];
+      L += mw == -INFINITY ? 0.f : sm.wl[w][tid] * exp2f(mw - M);
+    }
+    sm.m[tid] = M;
+    sm.l[tid] = L;
+  }
+  __syncthreads();
+  for (int w = 0; w < kDecWarps; ++w) {  // warps add in a fixed order: deterministic
+    if (w == warp) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = gq + 8 * h;
+        const float mw = F.m[h], M = sm.m[rr];
+        const float c = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+#pragma unroll
+        for (int d = 0; d < 16; ++d) {
+          const int col = d * 8 + 2 * (lane & 3);
+          sm.o[rr][col] += F.o[d][2 * h] * c;
+          sm.o[rr][col + 1] += F.o[d][2 * h + 1] * c;
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- merge the cluster over DSMEM: rank 0 writes the output ----
+  cluster.sync();
+  if (crank == 0 && !done) {
+    for (int idx = tid; idx < G * kHeadDim; idx += kDecWarps * 32) {
+      const int rr = idx / kHeadDim, d = idx % kHeadDim;
+      float M = -INFINITY;
+      for (int c = 0; c < kDecCluster; ++c) M = fmaxf(M, cluster.map_shared_rank(&sm, c)->m[rr]);
+      float L = 0.f, A = 0.f;
+      for (int c = 0; c < kDecCluster; ++c) {
+        const DecSmem* r = cluster.map_shared_rank(&sm, c);
+        const float mc = r->m[rr];
+        if (mc == -INFINITY) continue;
+        const float w = exp2f(mc - M);
+        L += r->l[rr] * w;
+        A += r->o[rr][d] * w;
+      }
+      p.out[(size_t)(g * G + rr) * kHeadDim + d] = __float2bfloat16_rn(L > 0.f ? A / L : 0.f);
+    }
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until rank 0 is done
+}
+
+cudaError_t attn_decode_tc_launch(const AttnParams& p, cudaStream_t stream, bool pdl) {
+  const int G = p.n_heads / p.n_kv;
+  if (G > 16) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_tc_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(DecSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_kv, kDecCluster, 1);
+  cfg.blockDim = dim3(kDecWarps * 32);
+  cfg.dynamicSmemBytes = sizeof(DecSmem);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr_l[1];
+  attr_l[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_l[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr_l;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, attn_decode_tc_kernel, p, G);
+}
+
+int attn_tc_splits(int n_kv, int q_tiles, int T, int num_sms) {
+  const int tiles = (T + kTile - 1) / kTile;
+  int s = num_sms / (n_kv * q_tiles);
+  if (s > tiles) s = tiles;
+  if (s > kAttnMaxSplit) s = kAttnMaxSplit;
+  return s < 1 ? 1 : s;
+}
+
+cudaError_t attn_tc_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream,
+                           bool pdl) {
+  const int G = p.n_heads / p.n_kv;
+  const int M_rows = M_tokens * G;
+  const int q_tiles = (M_rows + kRowsPerCta - 1) / kRowsPerCta;
+  if (nsplit > kAttnMaxSplit) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(TcaSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_kv, nsplit, q_tiles);
+  cfg.blockDim = dim3(kTcaThreads);
+  cfg.dynamicSmemBytes = sizeof(TcaSmem);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr_l[1];
+  attr_l[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_l[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr_l;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, attn_prefill_tc_kernel, p, M_rows, G);
+}
+
+}  // namespace sr

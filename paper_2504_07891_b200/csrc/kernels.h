@@ -91,6 +91,13 @@ struct AttnParams {
 };
 
 cudaError_t attn_decode_launch(const AttnParams& p, cudaStream_t stream, bool pdl);
+int attn_decode_splits(int n_kv, int num_sms);
+int attn_prefill_splits(int T);
+// tensor-core flash attention (attention_tc.cu)
+cudaError_t attn_decode_tc_launch(const AttnParams& p, cudaStream_t stream, bool pdl);
+cudaError_t attn_tc_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream,
+                           bool pdl);
+int attn_tc_splits(int n_kv, int q_tiles, int T, int num_sms);
 cudaError_t attn_prefill_launch(const AttnParams& p, int M, cudaStream_t stream);
 
 // ----------------------------------------------------------- prefill path ---

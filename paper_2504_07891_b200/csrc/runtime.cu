@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <vector>
 
@@ -39,7 +40,7 @@ static int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kPrefillSplitsMax = 8;
-constexpr int kAttnPrefillSplit = 8;
+constexpr int kAttnPrefillSplit = 16;
 
 struct Layout {  // workspace carve-up (byte offsets)
   size_t st, h, x, q, attn, act, part, apart, actr, lm_v1, lm_v2, lm_i1, lm_ctr, logits, ro_cnt,
@@ -56,7 +57,7 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
   const size_t qd = (size_t)d.n_heads * SR_HEAD_DIM;
   const size_t qkv = qd + 2 * (size_t)d.n_kv_heads * SR_HEAD_DIM;
   const size_t nmax = std::max<size_t>({qkv, (size_t)d.d_model, 2 * (size_t)d.d_ffn});
-  L.nsplit_decode = std::max(1, (2 * num_sms + d.n_kv_heads - 1) / d.n_kv_heads);
+  L.nsplit_decode = attn_decode_splits(d.n_kv_heads, num_sms);
   const size_t nsplit_max = std::max<size_t>(L.nsplit_decode, kAttnPrefillSplit);
   const size_t lm_parts = (size_t)gemv_max_grid(num_sms) + 64;
   size_t o = 0;
@@ -105,6 +106,8 @@ struct Model {
   sr_timing timing{};
   bool pdl = true;
   bool use_tc = true;  // tcgen05 GEMM (K6); SR_GEMM=mma selects the mma.sync reference
+  bool stream_decode = false;  // SR_DECODE=stream: per-token host loop (profiling only)
+  bool attn_simt = false;      // SR_ATTN=simt: CUDA-core split-KV attention (A/B reference)
   struct alignas(64) TMap { CUtensorMap m; };
   std::vector<TMap> wmaps;     // per layer: qkv, o, gu, d ; then lm_head
   TMap amaps[3][4];            // [x | attn | act][token tile 32/64/128/256]
@@ -186,7 +189,7 @@ struct Model {
       a.n_kv = d.n_kv_heads;
       a.nsplit = L.nsplit_decode;
       a.st = st;
-      e = attn_decode_launch(a, s, pdl);
+      e = attn_simt ? attn_decode_launch(a, s, pdl) : attn_decode_tc_launch(a, s, pdl);
       if (e != cudaSuccess) return e;
 
       p = gemv_base();
@@ -285,6 +288,7 @@ struct Model {
         ep.start_pos = pos0;
         ep.layer = l;
         SR_CK(epi_qkv_launch(ep, s));
+        watch(s, "qkv gemm+epi", l, M, last_splits);
         // attention
         AttnParams a{};
         a.q = q;
@@ -299,10 +303,18 @@ struct Model {
         a.n_heads = d.n_heads;
         a.n_kv = d.n_kv_heads;
         const int Tlast = pos0 + M;
-        a.nsplit = std::max(1, std::min(kAttnPrefillSplit, (Tlast + 255) / 256));
         a.start_pos = pos0;
         a.st = nullptr;
-        SR_CK(attn_prefill_launch(a, M, s));
+        if (attn_simt) {
+          a.nsplit = std::min(kAttnPrefillSplit, attn_prefill_splits(Tlast));
+          SR_CK(attn_prefill_launch(a, M, s));
+        } else {
+          const int G = d.n_heads / d.n_kv_heads;
+          const int q_tiles = (M * G + 63) / 64;
+          a.nsplit = std::min(kAttnPrefillSplit, attn_tc_splits(d.n_kv_heads, q_tiles, Tlast, num_sms));
+          SR_CK(attn_tc_launch(a, M, a.nsplit, s, false));
+          watch(s, "attn_prefill_tc", l, M, a.nsplit);
+        }
         // o-proj + residual + norm2
         rc = gemm(ACT_ATTN, l * 4 + 1, attn, lw(l, WO), M, d.d_model, q_dim, s);
         if (rc) return -rc;
@@ -314,6 +326,7 @@ struct Model {
         if (rc) return -rc;
         ep = epi_base(M, 2 * d.d_ffn);
         SR_CK(epi_glu_launch(ep, s));
+        watch(s, "o/gu gemm+epi", l, M, last_splits);
         // down + residual + next norm
         rc = gemm(ACT_ACT, l * 4 + 3, act, lw(l, WD), M, d.d_model, d.d_ffn, s);
         if (rc) return -rc;
@@ -327,6 +340,27 @@ struct Model {
   }
 
   int last_splits = 1;
+  // SR_WATCH=1: synchronise after each prefill stage and abort with the stage
+  // name if it does not finish within 10 s (bring-up aid for device hangs)
+  bool watch_on = false;
+  int watch_ms = 10000;
+  void watch(cudaStream_t s, const char* what, int layer, int M, int extra) {
+    if (!watch_on) return;
+    for (int i = 0; i < watch_ms; ++i) {
+      cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaSuccess) return;
+      if (e != cudaErrorNotReady) {
+        fprintf(stderr, "[sr watch] %s layer %d M %d extra %d: %s\n", what, layer, M, extra,
+                cudaGetErrorString(e));
+        abort();
+      }
+      struct timespec ts = {0, 1000000};
+      nanosleep(&ts, nullptr);
+    }
+    fprintf(stderr, "[sr watch] HANG in %s layer %d M %d extra %d\n", what, layer, M, extra);
+    abort();
+  }
+
   int gemm(int act_id, int wmap, const __nv_bfloat16* A, const __nv_bfloat16* B, int M, int N,
            int K, cudaStream_t s) {
     if (use_tc) {
@@ -466,6 +500,12 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
   for (auto& ev : m->ev) cudaEventCreate(&ev);
   if (const char* v = getenv("SR_NO_PDL")) m->pdl = (v[0] == '0');
   if (const char* v = getenv("SR_GEMM")) m->use_tc = strcmp(v, "mma") != 0;
+  if (const char* v = getenv("SR_DECODE")) m->stream_decode = strcmp(v, "stream") == 0;
+  if (const char* v = getenv("SR_ATTN")) m->attn_simt = strcmp(v, "simt") == 0;
+  if (const char* v = getenv("SR_WATCH")) {
+    m->watch_on = atoi(v) > 0;
+    m->watch_ms = atoi(v) > 1 ? atoi(v) * 1000 : 10000;
+  }
   if (int rc = m->build_tmaps()) {
     sr_model_destroy(m);
     return rc;
@@ -528,7 +568,20 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
   p.counter = m->lm_ctr;
   SR_CK(gemv_launch(GEMV_LM_ARGMAX_X, p, m->num_sms, s, false));
   SR_CK(cudaEventRecord(m->ev[1], s));
-  SR_CK(cudaGraphLaunch(m->exec, s));
+  if (!m->stream_decode) {
+    SR_CK(cudaGraphLaunch(m->exec, s));
+  } else {
+    // profiling mode (SR_DECODE=stream): same kernels launched per token from
+    // the host, so tools that cannot see into conditional graphs (ncu) can
+    SR_CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < max_new; ++i) {
+      int done = 0;
+      SR_CK(cudaMemcpy(&done, &m->st->done, sizeof(int), cudaMemcpyDeviceToHost));
+      if (done) break;
+      SR_CK(m->enqueue_decode_step(s));
+      SR_CK(cudaStreamSynchronize(s));
+    }
+  }
   SR_CK(cudaEventRecord(m->ev[2], s));
   m->timing.prefill_tokens = n_ids;
   m->timing.decode_tokens = -1;  // filled by the caller from out[0]
