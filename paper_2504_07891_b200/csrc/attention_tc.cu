@@ -360,21 +360,99 @@ __global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams
 
 // ----------------------------------------------------------------- decode --
 // One cluster of kDecCluster CTAs per KV head; the G query heads of the group
-// are the 16-row M tile.  KV tile i (64 positions) belongs to CTA i % C and,
-// inside it, to warp (i / C) % 4; each warp streams its tiles through a
-// private single-buffered K/V slot.  Warps merge (m, l, O) in shared memory,
-// then CTA rank 0 merges the cluster over DSMEM -- no global partials, no
-// atomics, no second kernel.
+// are the 16-row M tile.  KV tile i (64 positions = one page) belongs to CTA
+// i % C.  Inside a CTA all 128 threads stream the CTA's tiles through a
+// 2-stage cp.async ring and each warp takes a 16-position quarter of every
+// tile (S: 16 HMMA, PV: 32 HMMA with the hi/lo P split), keeping its own
+// online-softmax state.  Warps merge (m, l, O) in shared memory; the cluster
+// then merges over DSMEM with the work spread across its CTAs (CTA c writes
+// dims [16c, 16c + 16)) -- no global partials, no atomics, no extra kernel.
 constexpr int kDecCluster = 8;
 constexpr int kDecWarps = 4;
+constexpr int kDecStages = 2;
 
 struct DecSmem {
-  __align__(128) uint8_t kv[kDecWarps][2][kTileBytes];  // per-warp K, V
+  __align__(128) uint8_t k[kDecStages][kTileBytes];
+  __align__(128) uint8_t v[kDecStages][kTileBytes];
   __align__(128) uint8_t q[16 * kHeadDim * 2];
-  float o[16][kHeadDim];        // CTA-merged, unnormalised O (rescaled to m)
+  float o[16][kHeadDim];  // CTA-merged, unnormalised O (relative to m)
   float m[16], l[16];
   float wm[kDecWarps][16], wl[kDecWarps][16];
 };
+
+// one warp, 16 rows x 16 positions (quarter `sub` of a 64-position tile)
+template <bool CAUSAL>
+SR_DEV void flash_sub16(Flash& F, const uint32_t (&qa)[8][4], uint32_t ks, uint32_t vs, int lane,
+                        int sub, int tile_pos0, int lim) {
+  float s[2][4];
+#pragma unroll
+  for (int n = 0; n < 2; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int row = sub * 16 + ((lane >> 4) << 3) + (lane & 7);
+    const int chunk = kk * 2 + ((lane >> 3) & 1);
+    uint32_t b[4];
+    ldsm4(b, ks + swz(row, chunk));
+    mma_bf16(s[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[0], b[1]);
+    mma_bf16(s[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[2], b[3]);
+  }
+  const int t = lane & 3;
+  float mx0 = F.m[0], mx1 = F.m[1];
+#pragma unroll
+  for (int n = 0; n < 2; ++n) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[n][e] *= kScaleLog2;
+    if (CAUSAL) {
+      const int p0 = tile_pos0 + sub * 16 + n * 8 + 2 * t;
+      if (p0 > lim) { s[n][0] = -INFINITY; s[n][2] = -INFINITY; }
+      if (p0 + 1 > lim) { s[n][1] = -INFINITY; s[n][3] = -INFINITY; }
+    }
+    mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
+    mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
+  }
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+  const float base0 = mx0 == -INFINITY ? 0.f : mx0;
+  const float base1 = mx1 == -INFINITY ? 0.f : mx1;
+  const float c0 = exp2f(F.m[0] - base0), c1 = exp2f(F.m[1] - base1);
+  F.m[0] = mx0;
+  F.m[1] = mx1;
+  float rs0 = 0.f, rs1 = 0.f;
+  uint32_t pa[4], pl[4];
+#pragma unroll
+  for (int n = 0; n < 2; ++n) {
+    const float e0 = exp2f(s[n][0] - base0), e1 = exp2f(s[n][1] - base0);
+    const float e2 = exp2f(s[n][2] - base1), e3 = exp2f(s[n][3] - base1);
+    rs0 += e0 + e1;
+    rs1 += e2 + e3;
+    const uint32_t h01 = f2_to_bf2(e0, e1), h23 = f2_to_bf2(e2, e3);
+    const float2 r01 = bf2_to_f2(h01), r23 = bf2_to_f2(h23);
+    pa[2 * n] = h01;
+    pa[2 * n + 1] = h23;
+    pl[2 * n] = f2_to_bf2(e0 - r01.x, e1 - r01.y);
+    pl[2 * n + 1] = f2_to_bf2(e2 - r23.x, e3 - r23.y);
+  }
+  F.l[0] = F.l[0] * c0 + rs0;
+  F.l[1] = F.l[1] * c1 + rs1;
+#pragma unroll
+  for (int d = 0; d < 16; ++d) {
+    F.o[d][0] *= c0; F.o[d][1] *= c0;
+    F.o[d][2] *= c1; F.o[d][3] *= c1;
+  }
+#pragma unroll
+  for (int dp = 0; dp < 8; ++dp) {
+    const int row = sub * 16 + (((lane >> 3) & 1) << 3) + (lane & 7);
+    const int chunk = dp * 2 + (lane >> 4);
+    uint32_t b[4];
+    ldsm4t(b, vs + swz(row, chunk));
+    mma_bf16(F.o[2 * dp], pa[0], pa[1], pa[2], pa[3], b[0], b[1]);
+    mma_bf16(F.o[2 * dp + 1], pa[0], pa[1], pa[2], pa[3], b[2], b[3]);
+    mma_bf16(F.o[2 * dp], pl[0], pl[1], pl[2], pl[3], b[0], b[1]);
+    mma_bf16(F.o[2 * dp + 1], pl[0], pl[1], pl[2], pl[3], b[2], b[3]);
+  }
+}
 
 __global__ void __cluster_dims__(1, kDecCluster, 1) __launch_bounds__(kDecWarps * 32)
     attn_decode_tc_kernel(AttnParams p, int G) {
@@ -385,7 +463,7 @@ __global__ void __cluster_dims__(1, kDecCluster, 1) __launch_bounds__(kDecWarps 
 
   grid_launch_dependents();
   grid_wait();
-  const bool done = p.st->done != 0;  // uniform across the cluster
+  const bool done = p.st->done != 0;  // same for every CTA of the launch
 
   const int g = blockIdx.x;
   const int crank = (int)cluster.block_rank();
@@ -402,42 +480,46 @@ __global__ void __cluster_dims__(1, kDecCluster, 1) __launch_bounds__(kDecWarps 
     const int T = p.st->ctx_len;
     const int* ptab = p.st->page_table;
     const int n_tiles = (T + kTile - 1) / kTile;
-    // Q (G rows) -> smem, rows >= G zero
-    const uint32_t qs = s_u32(sm.q);
+    const int n_mine = n_tiles > crank ? (n_tiles - crank + kDecCluster - 1) / kDecCluster : 0;
+    auto issue = [&](int j, int stage) {
+      const int i = crank + j * kDecCluster;
+      const size_t off = kv_offset(p.layer, ptab[i], g, 0, p.n_pages, p.n_kv);
+      const uint8_t* kg = reinterpret_cast<const uint8_t*>(p.k_pool + off);
+      const uint8_t* vg = reinterpret_cast<const uint8_t*>(p.v_pool + off);
+      const uint32_t kb = s_u32(sm.k[stage]), vb = s_u32(sm.v[stage]);
+#pragma unroll
+      for (int c = tid; c < kTile * 16; c += kDecWarps * 32) {
+        const int r = c >> 4, ch = c & 15;
+        cpa16(kb + swz(r, ch), kg + r * 256 + ch * 16);
+        cpa16(vb + swz(r, ch), vg + r * 256 + ch * 16);
+      }
+    };
+    if (n_mine > 0) issue(0, 0);
+    cpa_commit();
     for (int i = tid; i < 16 * 16; i += kDecWarps * 32) {
       const int r = i >> 4, c = i & 15;
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < G) {
-        v = reinterpret_cast<const uint4*>(p.q + (size_t)(g * G + r) * kHeadDim)[c];
-      }
+      if (r < G) v = reinterpret_cast<const uint4*>(p.q + (size_t)(g * G + r) * kHeadDim)[c];
       *reinterpret_cast<uint4*>(sm.q + swz(r, c)) = v;
     }
     __syncthreads();
     uint32_t qa[8][4];
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) ldsm4(qa[kk], qs + swz(lane & 15, kk * 2 + (lane >> 4)));
-
-    const uint32_t ks = s_u32(sm.kv[warp][0]), vs = s_u32(sm.kv[warp][1]);
+    for (int kk = 0; kk < 8; ++kk) ldsm4(qa[kk], s_u32(sm.q) + swz(lane & 15, kk * 2 + (lane >> 4)));
     const int lim = T - 1;
-    for (int i = crank + kDecCluster * warp; i < n_tiles; i += kDecCluster * kDecWarps) {
-      const int page = ptab[i];
-      const size_t off = kv_offset(p.layer, page, g, 0, p.n_pages, p.n_kv);
-      const uint8_t* kg = reinterpret_cast<const uint8_t*>(p.k_pool + off);
-      const uint8_t* vg = reinterpret_cast<const uint8_t*>(p.v_pool + off);
-#pragma unroll 4
-      for (int j = lane; j < kTile * 16; j += 32) {
-        const int r = j >> 4, c = j & 15;
-        cpa16(ks + swz(r, c), kg + r * 256 + c * 16);
-        cpa16(vs + swz(r, c), vg + r * 256 + c * 16);
-      }
+    for (int j = 0; j < n_mine; ++j) {
+      const int stage = j & 1;
+      if (j + 1 < n_mine) issue(j + 1, stage ^ 1);
       cpa_commit();
-      cpa_wait<0>();
-      __syncwarp();
-      const int pos0 = i * kTile;
-      if (pos0 + kTile - 1 > lim) flash_tile<true>(F, qa, ks, vs, lane, pos0, lim, lim);
-      else flash_tile<false>(F, qa, ks, vs, lane, pos0, lim, lim);
-      __syncwarp();
+      cpa_wait<1>();
+      __syncthreads();
+      const int pos0 = (crank + j * kDecCluster) * kTile;
+      const uint32_t ks = s_u32(sm.k[stage]), vs = s_u32(sm.v[stage]);
+      if (pos0 + kTile - 1 > lim) flash_sub16<true>(F, qa, ks, vs, lane, warp, pos0, lim);
+      else flash_sub16<false>(F, qa, ks, vs, lane, warp, pos0, lim);
+      __syncthreads();
     }
+    cpa_wait<0>();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       F.l[h] += __shfl_xor_sync(0xffffffffu, F.l[h], 1);
@@ -445,7 +527,7 @@ __global__ void __cluster_dims__(1, kDecCluster, 1) __launch_bounds__(kDecWarps 
     }
   }
 
-  // ---- merge the 4 warps of this CTA ----
+  // ---- merge the 4 warps of this CTA (fixed order: deterministic) ----
   if ((lane & 3) == 0) {
     sm.wm[warp][gq] = F.m[0];
     sm.wm[warp][gq + 8] = F.m[1];
@@ -465,7 +547,7 @@ __global__ void __cluster_dims__(1, kDecCluster, 1) __launch_bounds__(kDecWarps 
     sm.l[tid] = L;
   }
   __syncthreads();
-  for (int w = 0; w < kDecWarps; ++w) {  // warps add in a fixed order: deterministic
+  for (int w = 0; w < kDecWarps; ++w) {
     if (w == warp) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -483,26 +565,32 @@ __global__ void __cluster_dims__(1, kDecCluster, 1) __launch_bounds__(kDecWarps 
     __syncthreads();
   }
 
-  // ---- merge the cluster over DSMEM: rank 0 writes the output ----
+  // ---- cluster merge over DSMEM, spread over the CTAs: CTA c writes dims [16c, 16c+16) ----
   cluster.sync();
-  if (crank == 0 && !done) {
-    for (int idx = tid; idx < G * kHeadDim; idx += kDecWarps * 32) {
-      const int rr = idx / kHeadDim, d = idx % kHeadDim;
+  if (!done) {
+    constexpr int kDims = kHeadDim / kDecCluster;
+    for (int idx = tid; idx < G * kDims; idx += kDecWarps * 32) {
+      const int rr = idx / kDims, d = crank * kDims + idx % kDims;
+      float mc[kDecCluster];
       float M = -INFINITY;
-      for (int c = 0; c < kDecCluster; ++c) M = fmaxf(M, cluster.map_shared_rank(&sm, c)->m[rr]);
-      float L = 0.f, A = 0.f;
+#pragma unroll
       for (int c = 0; c < kDecCluster; ++c) {
+        mc[c] = cluster.map_shared_rank(&sm, c)->m[rr];
+        M = fmaxf(M, mc[c]);
+      }
+      float L = 0.f, A = 0.f;
+#pragma unroll
+      for (int c = 0; c < kDecCluster; ++c) {
+        if (mc[c] == -INFINITY) continue;
         const DecSmem* r = cluster.map_shared_rank(&sm, c);
-        const float mc = r->m[rr];
-        if (mc == -INFINITY) continue;
-        const float w = exp2f(mc - M);
+        const float w = exp2f(mc[c] - M);
         L += r->l[rr] * w;
         A += r->o[rr][d] * w;
       }
       p.out[(size_t)(g * G + rr) * kHeadDim + d] = __float2bfloat16_rn(L > 0.f ? A / L : 0.f);
     }
   }
-  cluster.sync();  // keep every CTA's shared memory alive until rank 0 is done
+  cluster.sync();  // keep every CTA's shared memory alive until all reads are done
 }
 
 cudaError_t attn_decode_tc_launch(const AttnParams& p, cudaStream_t stream, bool pdl) {

@@ -3,12 +3,18 @@
 // append, residual add, SiLU*up, greedy argmax + stop test).
 //
 // Layout: W is row-major [N, K] bf16 (out_features x in_features).  A CTA of
-// 8 warps stages the input vector x (bf16, K elements) in shared memory; every
-// warp owns a "task" of ROWS rows and streams them with 16-byte
-// ld.global.nc.L1::no_allocate loads, U chunks of 256 elements in flight per
-// row, fp32 accumulation and a warp-shuffle reduction.  Grids are at most one
-// wave (grid-stride over tasks) so that programmatic dependent launch can start
-// the next kernel's weight prefetch on the free slots while this one drains.
+// 8 warps stages the input vector x (bf16, K elements) in shared memory.  The
+// CTA's warps form RG = 8 / KS row groups of KS warps; a row group owns a task
+// of ROWS rows and its KS warps each stream one K-slice of those rows.
+//
+// Each warp walks a flat sequence of load batches (task, U chunks of 256
+// elements) with two register buffers: batch b+1 is in flight while batch b is
+// consumed, across task boundaries, so every warp keeps U*ROWS 16-byte
+// ld.global.nc.L1::no_allocate loads outstanding for its whole lifetime.  The
+// first batch depends only on the (constant) weights and is issued *before*
+// the programmatic-dependent-launch wait, overlapping the previous kernel's
+// tail.  fp32 accumulation, warp-shuffle reduction and, for KS > 1, a
+// fixed-order shared-memory reduction of the K slices (deterministic).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -19,7 +25,9 @@ enum { EPI_QKV = 0, EPI_RESID = 1, EPI_GLU = 2, EPI_ARGMAX = 3, EPI_LOGITS = 4 }
 
 constexpr int kGemvThreads = 256;
 constexpr int kGemvWarps = kGemvThreads / 32;
-constexpr int kChunk = 256;  // elements per warp-wide 16-byte load
+constexpr int kChunk = 256;            // elements per warp-wide 16-byte load
+constexpr int kNormMax = 5120 / kGemvThreads;  // h elements per thread (d <= 5120)
+constexpr int kMaxIters = 32;          // K-split kernels: tasks per row group per CTA
 
 template <int ROWS>
 SR_DEV void task_rows(int epi, int task, const GemvParams& p, int (&r)[ROWS]) {
@@ -47,30 +55,58 @@ SR_DEV void task_rows(int epi, int task, const GemvParams& p, int (&r)[ROWS]) {
   }
 }
 
-template <int IN, int EPI, int ROWS, int U>
+template <int IN, int EPI, int ROWS, int U, int KS>
 __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   __shared__ float red[32];
+  __shared__ float kpart[KS > 1 ? kMaxIters : 1][kGemvWarps / KS][KS];
   __shared__ float s_v1[kGemvWarps], s_v2[kGemvWarps];
   __shared__ int s_i1[kGemvWarps];
   __shared__ bool s_last;
+  constexpr int RG = kGemvWarps / KS;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rg = warp / KS, ks = warp % KS;
   const int K = p.K;
   const int n_tasks = p.n_tasks;
-  const int stride = gridDim.x * kGemvWarps;
   const int nchunk = (K + kChunk - 1) / kChunk;
+  const int c_per = (nchunk + KS - 1) / KS;  // chunks of this warp's K slice
+  const int c_lo = ks * c_per;
+  const int c_hi = min(nchunk, c_lo + c_per);
+  const int nb = c_hi > c_lo ? (c_hi - c_lo + U - 1) / U : 1;  // load batches per task
+  const int stride = gridDim.x * RG;
+  const int task0 = blockIdx.x * RG + rg;
+  const int iters = (n_tasks + stride - 1) / stride;  // per CTA (uniform)
+  const int my_iters = task0 < n_tasks ? (n_tasks - task0 + stride - 1) / stride : 0;
+  const int total = my_iters * nb;
 
-  // ---- weight prefetch of the first task (independent of predecessors) ----
-  int task = blockIdx.x * kGemvWarps + warp;
-  if (task < n_tasks) {
+  uint4 wa[ROWS][U], wb[ROWS][U];
+  auto load = [&](int B, uint4 (&w)[ROWS][U]) {
+    const int task = task0 + (B / nb) * stride;
+    const int c0 = c_lo + (B % nb) * U;
     int r[ROWS];
     task_rows<ROWS>(EPI, task, p, r);
 #pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = (c0 + u) * kChunk + lane * 8;
+      const bool ok = (c0 + u < c_hi) && k < K;
+#pragma unroll
+      for (int i = 0; i < ROWS; ++i)
+        w[i][u] = ok ? ld_stream(p.W + (size_t)r[i] * K + k) : make_uint4(0, 0, 0, 0);
+    }
+  };
+
+  // ---- first weight batch: independent of every predecessor ----
+  if (total > 0) load(0, wa);
+  if (p.prefetch && total > 1) {
+    int r[ROWS];
+    task_rows<ROWS>(EPI, task0, p, r);
+#pragma unroll
     for (int i = 0; i < ROWS; ++i) {
       const char* row = reinterpret_cast<const char*>(p.W + (size_t)r[i] * K);
-      for (int off = lane * 128; off < K * 2; off += 32 * 128) prefetch_l2(row + off);
+      for (int c = c_lo + U + lane / 4; c < c_hi; c += 8)
+        prefetch_l2(row + c * kChunk * 2 + (lane & 3) * 128);
     }
   }
   grid_launch_dependents();
@@ -84,22 +120,30 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
     for (int i = threadIdx.x; i < K / 8; i += kGemvThreads)
       reinterpret_cast<uint4*>(xs)[i] = src[i];
   } else {
-    const float* hin = p.h;
+    // RMSNorm of h (or of the embedding row): one read, values kept in registers
+    float hv[kNormMax];
     const __nv_bfloat16* erow = nullptr;
     if constexpr (IN == IN_EMBED_NORM) erow = p.embed + (size_t)st->token * K;
     float ss = 0.f;
-    for (int i = threadIdx.x; i < K; i += kGemvThreads) {
-      float v = (IN == IN_EMBED_NORM) ? bf_to_f(erow[i]) : hin[i];
+#pragma unroll
+    for (int j = 0; j < kNormMax; ++j) {
+      const int i = threadIdx.x + j * kGemvThreads;
+      float v = 0.f;
+      if (i < K) v = (IN == IN_EMBED_NORM) ? bf_to_f(erow[i]) : p.h[i];
+      hv[j] = v;
       ss += v * v;
     }
     ss = block_sum(ss, red);
     const float rstd = rsqrtf(ss / K + p.eps);
-    for (int i = threadIdx.x; i < K; i += kGemvThreads) {
-      float v = (IN == IN_EMBED_NORM) ? bf_to_f(erow[i]) : hin[i];
-      if constexpr (IN == IN_EMBED_NORM) {
-        if (blockIdx.x == 0) p.h[i] = v;  // residual stream starts at the embedding
+#pragma unroll
+    for (int j = 0; j < kNormMax; ++j) {
+      const int i = threadIdx.x + j * kGemvThreads;
+      if (i < K) {
+        if constexpr (IN == IN_EMBED_NORM) {
+          if (blockIdx.x == 0) p.h[i] = hv[j];  // residual stream starts at the embedding
+        }
+        xs[i] = __float2bfloat16_rn(hv[j] * rstd * bf_to_f(p.norm_w[i]));
       }
-      xs[i] = __float2bfloat16_rn(v * rstd * bf_to_f(p.norm_w[i]));
     }
   }
   __syncthreads();
@@ -107,37 +151,20 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
   Top2 best;
   best.init();
   const uint4* xs4 = reinterpret_cast<const uint4*>(xs);
+  float acc[ROWS];
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) acc[i] = 0.f;
 
-  for (; task < n_tasks; task += stride) {
-    int r[ROWS];
-    task_rows<ROWS>(EPI, task, p, r);
-    float acc[ROWS];
-#pragma unroll
-    for (int i = 0; i < ROWS; ++i) acc[i] = 0.f;
-    for (int c0 = 0; c0 < nchunk; c0 += U) {
-      uint4 w[ROWS][U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = (c0 + u) * kChunk + lane * 8;
-#pragma unroll
-        for (int i = 0; i < ROWS; ++i)
-          w[i][u] = (c0 + u < nchunk && k < K) ? ld_stream(p.W + (size_t)r[i] * K + k)
-                                               : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = (c0 + u) * kChunk + lane * 8;
-        if (c0 + u < nchunk && k < K) {
-          const uint4 xv = xs4[k / 8];
-#pragma unroll
-          for (int i = 0; i < ROWS; ++i) acc[i] = dot8(w[i][u], xv, acc[i]);
-        }
-      }
-    }
+  auto finish = [&](int it) {
+    const int task = task0 + it * stride;
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) acc[i] = warp_sum(acc[i]);
-
-    if (lane == 0) {
+    if constexpr (KS > 1) {
+      // park the K-slice partial; the CTA reduces all of them after the loop
+      if (lane == 0 && it < kMaxIters) kpart[it][rg][ks] = acc[0];
+    } else if (lane == 0) {
+      int r[ROWS];
+      task_rows<ROWS>(EPI, task, p, r);
       if constexpr (EPI == EPI_RESID) {
 #pragma unroll
         for (int i = 0; i < ROWS; ++i) p.h[r[i]] += acc[i];
@@ -150,12 +177,11 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
           if (r[i] < p.n_valid) best.push(acc[i], r[i]);
       } else if constexpr (EPI == EPI_GLU) {
         const float g = acc[0], u = acc[1];
-        const float a = g / (1.f + __expf(-g)) * u;
-        p.act_out[task] = __float2bfloat16_rn(a);
+        p.act_out[task] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
       } else if constexpr (EPI == EPI_QKV) {
         const int pos = st->pos;
-        float v0 = acc[0] + bf_to_f(p.bias[r[0]]);
-        float v1 = acc[1] + bf_to_f(p.bias[r[1]]);
+        const float v0 = acc[0] + bf_to_f(p.bias[r[0]]);
+        const float v1 = acc[1] + bf_to_f(p.bias[r[1]]);
         const int qk = p.q_dim + p.kv_dim;
         if (r[0] < qk) {
           const int j = r[0] % kHeadDim;  // < 64
@@ -183,6 +209,49 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
         }
       }
     }
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) acc[i] = 0.f;
+  };
+
+  auto consume = [&](int B, const uint4 (&w)[ROWS][U]) {
+    const int cb = B % nb;
+    const int c0 = c_lo + cb * U;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = (c0 + u) * kChunk + lane * 8;
+      if (c0 + u < c_hi && k < K) {
+        const uint4 xv = xs4[k / 8];
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) acc[i] = dot8(w[i][u], xv, acc[i]);
+      }
+    }
+    if (cb == nb - 1) finish(B / nb);
+  };
+
+  // ---- software-pipelined stream: two register buffers ----
+  for (int B = 0; B < total; B += 2) {
+    if (B + 1 < total) load(B + 1, wb);
+    consume(B, wa);
+    if (B + 1 < total) {
+      if (B + 2 < total) load(B + 2, wa);
+      consume(B + 1, wb);
+    }
+  }
+
+  if constexpr (KS > 1) {
+    // fixed-order reduction of the K-slice partials, then the residual epilogue
+    static_assert(EPI == EPI_RESID && ROWS == 1, "K-split is for residual GEMVs");
+    __syncthreads();
+    const int n_out = min(iters, kMaxIters) * RG;
+    for (int o = threadIdx.x; o < n_out; o += kGemvThreads) {
+      const int oit = o / RG, org = o % RG;
+      const int task = blockIdx.x * RG + org + oit * stride;
+      if (task >= n_tasks) continue;
+      float s = 0.f;
+#pragma unroll
+      for (int j = 0; j < KS; ++j) s += kpart[oit][org][j];
+      p.h[task] += s;
+    }
   }
 
   if constexpr (EPI == EPI_ARGMAX) {
@@ -205,9 +274,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
       __threadfence();
       Top2 b;
       b.init();
-      for (int i = threadIdx.x; i < (int)gridDim.x; i += kGemvThreads) {
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += kGemvThreads)
         b.merge(__ldcg(p.part_v1 + i), __ldcg(p.part_i1 + i), __ldcg(p.part_v2 + i));
-      }
       warp_top2(b);
       if (lane == 0) { s_v1[warp] = b.v1; s_v2[warp] = b.v2; s_i1[warp] = b.i1; }
       __syncthreads();
@@ -223,10 +291,10 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
 }
 
 // ------------------------------------------------------------- launchers ---
-template <int IN, int EPI, int ROWS, int U>
+template <int IN, int EPI, int ROWS, int U, int KS>
 static cudaError_t launch(const GemvParams& p, int grid, cudaStream_t stream, bool pdl) {
   const int smem = ((p.K * 2 + 15) / 16) * 16;
-  auto fn = gemv_kernel<IN, EPI, ROWS, U>;
+  auto fn = gemv_kernel<IN, EPI, ROWS, U, KS>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
@@ -246,39 +314,100 @@ static cudaError_t launch(const GemvParams& p, int grid, cudaStream_t stream, bo
   return cudaLaunchKernelEx(&cfg, fn, p);
 }
 
-static int grid_for(int n_tasks, int num_sms, int per_sm) {
-  int g = (n_tasks + kGemvWarps - 1) / kGemvWarps;
-  const int cap = num_sms * per_sm;
+static int gemv_per_sm() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_GEMV_PER_SM");
+    v = e ? atoi(e) : 4;
+    if (v < 1 || v > 4) v = 4;
+  }
+  return v;
+}
+
+static int grid_for(int n_tasks, int rows_per_cta, int num_sms) {
+  int g = (n_tasks + rows_per_cta - 1) / rows_per_cta;
+  const int cap = num_sms * gemv_per_sm();
   return g < cap ? g : cap;
 }
 
+// chunks per load batch: SR_GEMV_U (pair kernels) / SR_GEMV_UR (residual) tune
+static int env_u(const char* name, int dflt) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : dflt;
+  return (v == 2 || v == 4 || v == 8) ? v : dflt;
+}
+
+template <int IN, int EPI, int ROWS, int U>
+static cudaError_t launch1(GemvParams p, int num_sms, cudaStream_t stream, bool pdl) {
+  static const int u = env_u("SR_GEMV_U", U);
+  const int grid = grid_for(p.n_tasks, kGemvWarps, num_sms);
+  if (u == 8) return launch<IN, EPI, ROWS, 8, 1>(p, grid, stream, pdl);
+  if (u == 2) return launch<IN, EPI, ROWS, 2, 1>(p, grid, stream, pdl);
+  return launch<IN, EPI, ROWS, 4, 1>(p, grid, stream, pdl);
+}
+
+template <int U>
+static cudaError_t launch_resid_u(GemvParams p, int ks, int num_sms, cudaStream_t stream, bool pdl) {
+  switch (ks) {
+    case 1: return launch<IN_X, EPI_RESID, 1, U, 1>(p, grid_for(p.n_tasks, kGemvWarps, num_sms), stream, pdl);
+    case 2: return launch<IN_X, EPI_RESID, 1, U, 2>(p, grid_for(p.n_tasks, kGemvWarps / 2, num_sms), stream, pdl);
+    case 4: return launch<IN_X, EPI_RESID, 1, U, 4>(p, grid_for(p.n_tasks, kGemvWarps / 4, num_sms), stream, pdl);
+    default: return launch<IN_X, EPI_RESID, 1, U, 8>(p, grid_for(p.n_tasks, 1, num_sms), stream, pdl);
+  }
+}
+
+static cudaError_t launch_resid(GemvParams p, int ks, int num_sms, cudaStream_t stream, bool pdl) {
+  static const int u = env_u("SR_GEMV_UR", 4);
+  if (u == 8) return launch_resid_u<8>(p, ks, num_sms, stream, pdl);
+  if (u == 2) return launch_resid_u<2>(p, ks, num_sms, stream, pdl);
+  return launch_resid_u<4>(p, ks, num_sms, stream, pdl);
+}
+
+// K-split for one-row-per-task residual GEMVs: split while the chip has fewer
+// than ~4 row tasks per warp slot and each slice keeps >= 4 chunks per warp
+static int pick_ks(int rows, int K, int num_sms) {
+  const int slots = num_sms * gemv_per_sm() * kGemvWarps;
+  const int nchunk = K / kChunk;
+  int ks = 1;
+  while (ks < 8 && (long)rows * ks < 4L * slots && nchunk / (ks * 2) >= 4) ks *= 2;
+  return ks;
+}
+
 cudaError_t gemv_launch(GemvKind kind, GemvParams p, int num_sms, cudaStream_t stream, bool pdl) {
+  if (p.K > 5120 && (kind == GEMV_QKV || kind == GEMV_QKV_EMBED || kind == GEMV_GLU ||
+                     kind == GEMV_LM_ARGMAX))
+    return cudaErrorInvalidValue;  // RMSNorm prologue keeps d <= 5120 values in registers
   switch (kind) {
     case GEMV_QKV_EMBED:
       p.n_tasks = p.N / 2;
-      return launch<IN_EMBED_NORM, EPI_QKV, 2, 4>(p, grid_for(p.n_tasks, num_sms, 2), stream, pdl);
+      return launch1<IN_EMBED_NORM, EPI_QKV, 2, 4>(p, num_sms, stream, pdl);
     case GEMV_QKV:
       p.n_tasks = p.N / 2;
-      return launch<IN_H_NORM, EPI_QKV, 2, 4>(p, grid_for(p.n_tasks, num_sms, 2), stream, pdl);
-    case GEMV_RESID:
+      return launch1<IN_H_NORM, EPI_QKV, 2, 4>(p, num_sms, stream, pdl);
+    case GEMV_RESID: {
       p.n_tasks = p.N;
-      return launch<IN_X, EPI_RESID, 1, 8>(p, grid_for(p.n_tasks, num_sms, 2), stream, pdl);
+      int ks = pick_ks(p.N, p.K, num_sms);
+      const int rg = kGemvWarps / ks;
+      const int grid = grid_for(p.N, rg, num_sms);
+      if ((p.N + grid * rg - 1) / (grid * rg) > kMaxIters) ks = 1;  // partial buffer bound
+      return launch_resid(p, ks, num_sms, stream, pdl);
+    }
     case GEMV_GLU:
       p.n_tasks = p.N / 2;
-      return launch<IN_H_NORM, EPI_GLU, 2, 4>(p, grid_for(p.n_tasks, num_sms, 2), stream, pdl);
+      return launch1<IN_H_NORM, EPI_GLU, 2, 4>(p, num_sms, stream, pdl);
     case GEMV_LM_ARGMAX:
       p.n_tasks = (p.n_valid + 1) / 2;
-      return launch<IN_H_NORM, EPI_ARGMAX, 2, 4>(p, grid_for(p.n_tasks, num_sms, 2), stream, pdl);
+      return launch1<IN_H_NORM, EPI_ARGMAX, 2, 4>(p, num_sms, stream, pdl);
     case GEMV_LM_ARGMAX_X:
       p.n_tasks = (p.n_valid + 1) / 2;
-      return launch<IN_X, EPI_ARGMAX, 2, 4>(p, grid_for(p.n_tasks, num_sms, 2), stream, pdl);
+      return launch1<IN_X, EPI_ARGMAX, 2, 4>(p, num_sms, stream, pdl);
     case GEMV_LM_LOGITS_X:
       p.n_tasks = (p.N + 1) / 2;
-      return launch<IN_X, EPI_LOGITS, 2, 4>(p, grid_for(p.n_tasks, num_sms, 2), stream, pdl);
+      return launch1<IN_X, EPI_LOGITS, 2, 4>(p, num_sms, stream, pdl);
   }
   return cudaErrorInvalidValue;
 }
 
-int gemv_max_grid(int num_sms) { return num_sms * 2; }
+int gemv_max_grid(int num_sms) { return num_sms * 4; }
 
 }  // namespace sr

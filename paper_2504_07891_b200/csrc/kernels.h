@@ -39,6 +39,7 @@ struct GemvParams {
   float* part_v2;
   int* part_i1;
   unsigned int* counter;
+  int prefetch;  // issue L2 prefetches of the first task before the dependency wait
   DecodeState* st;
 };
 

@@ -108,6 +108,7 @@ struct Model {
   bool use_tc = true;  // tcgen05 GEMM (K6); SR_GEMM=mma selects the mma.sync reference
   bool stream_decode = false;  // SR_DECODE=stream: per-token host loop (profiling only)
   bool attn_simt = false;      // SR_ATTN=simt: CUDA-core split-KV attention (A/B reference)
+  bool prefetch = false;       // SR_PREFETCH=1: GEMV L2 prefetch before the PDL wait
   struct alignas(64) TMap { CUtensorMap m; };
   std::vector<TMap> wmaps;     // per layer: qkv, o, gu, d ; then lm_head
   TMap amaps[3][4];            // [x | attn | act][token tile 32/64/128/256]
@@ -157,6 +158,7 @@ struct Model {
     p.kv_dim = kv_dim;
     p.h = h;
     p.st = st;
+    p.prefetch = prefetch ? 1 : 0;
     return p;
   }
 
@@ -502,6 +504,7 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
   if (const char* v = getenv("SR_GEMM")) m->use_tc = strcmp(v, "mma") != 0;
   if (const char* v = getenv("SR_DECODE")) m->stream_decode = strcmp(v, "stream") == 0;
   if (const char* v = getenv("SR_ATTN")) m->attn_simt = strcmp(v, "simt") == 0;
+  if (const char* v = getenv("SR_PREFETCH")) m->prefetch = v[0] == '1';
   if (const char* v = getenv("SR_WATCH")) {
     m->watch_on = atoi(v) > 0;
     m->watch_ms = atoi(v) > 1 ? atoi(v) * 1000 : 10000;
