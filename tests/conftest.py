@@ -8,6 +8,9 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 REFERENCE_SRC = Path("/root/reference/pkg/src")
+# the unmodified reference installed by `pip install --target baseline/_ref`
+# (travels to the GPU box, where /root/reference does not exist)
+REFERENCE_INSTALL = ROOT / "baseline" / "_ref"
 
 
 def pytest_configure(config):
@@ -15,17 +18,25 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+def reference_root() -> Path | None:
+    for root in (REFERENCE_SRC, REFERENCE_INSTALL):
+        if (root / "stepspec" / "__init__.py").exists():
+            return root
+    return None
+
+
 def reference_available() -> bool:
-    return (REFERENCE_SRC / "stepspec" / "__init__.py").exists()
+    return reference_root() is not None
 
 
 @pytest.fixture(scope="session")
 def stepspec():
     """The unmodified reference package (read-only import), when present."""
-    if not reference_available():
-        pytest.skip("reference package not mounted")
-    if str(REFERENCE_SRC) not in sys.path:
-        sys.path.insert(0, str(REFERENCE_SRC))
+    root = reference_root()
+    if root is None:
+        pytest.skip("reference package neither mounted nor installed in baseline/_ref")
+    if str(root) not in sys.path:
+        sys.path.insert(0, str(root))
     import stepspec as mod
 
     return mod
