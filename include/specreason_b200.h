@@ -163,6 +163,22 @@ int sr_forward_logits(void* model, const int32_t* page_table, int32_t start_pos,
 /* device timings of the last sr_generate / sr_score on this model */
 int sr_last_timing(void* model, sr_timing* h_out);
 
+/*
+ * Profiling hook: with SR_MK_PROF=1 in the environment at sr_model_create,
+ * the persistent decode kernel records globaltimer stamps (ns) of CTA 0 after
+ * every phase of the first decoded token of each sr_generate; copies the
+ * first n (<= 2048) of them to h_out.
+ */
+int sr_debug_profile(void* model, uint64_t* h_out, int32_t n);
+
+/*
+ * Bring-up hook: with SR_MK_TRACE=1 at sr_model_create, every CTA of the
+ * persistent decode kernel publishes progress words (step, stages consumed,
+ * barrier target, stages issued, tokens) to mapped host memory [#SMs][8];
+ * readable (no CUDA call) even while a kernel hangs.
+ */
+int sr_debug_trace(void* model, int32_t* h_out, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -126,7 +126,7 @@ struct DecodeState {
   int finish;       // SR_FINISH_*
   int max_new;
   int ctx_len;      // pos + 1: K/V length the attention reads
-  int pad0;
+  unsigned bar;     // grid-barrier counter of the persistent decode kernel (reset per call)
   const int* page_table;
   const uint8_t* token_class;
   int* out_ids;     // caller's out + 2

@@ -1,0 +1,913 @@
+// Persistent weight-streaming decode kernel: K1 + K3 + K4 + K5 + K10 fused.
+//
+// One launch decodes a whole reasoning step (every token until a stop-class
+// token, </think> or max_new).  One CTA per SM (grid = #SMs, cooperative
+// launch so all CTAs are co-resident); each CTA has
+//
+//   * a producer warp: one lane streams the CTA's share of every weight matrix
+//     of the model -- layer 0 qkv, o, gate/up, down, layer 1 ..., LM head, then
+//     the next token's layer 0 ... -- as 32-row x 256-column bf16 tiles (16 KB)
+//     through a TMA (cp.async.bulk.tensor) + mbarrier ring of up to 13 stages
+//     (~200 KB in flight per SM).  Weights are constant, so the producer never
+//     waits for activations: it runs ahead across phase and grid barriers and
+//     even into the next token, bounded only by the ring.  HBM streaming
+//     therefore does not stop while the consumers synchronise;
+//   * 16 consumer warps that run the token's phases in order, separated by
+//     grid barriers (one atomic counter, acquire/release):
+//
+//       per layer: QKV | ATTN | COMBINE | O | GATE/UP | DOWN      then: LM head
+//
+// GEMV phases.  A phase's tiles ("units", row-block major, k minor) are cut
+// into G contiguous ranges, one per CTA, so every CTA streams the same number
+// of bytes (+-1 tile).  Warp w of a tile owns rows w and w+16 (lane = 8
+// columns, one 16-byte shared load per row); partial dot products stay in
+// registers across the k tiles of a row block and are reduced once per block
+// with warp shuffles.  A row block cut by a range boundary leaves one partial
+// per contributing CTA in `part[cta][j][32]`; the next phase's prologue sums
+// the 1-3 partials of each row in CTA order (deterministic, no atomics).
+// GATE/UP and LM head use block-granular ranges instead: the interleaved
+// gate/up layout (16 gate rows then the 16 matching up rows per 32-row block)
+// lets the gate/up epilogue emit silu(g)*u directly, and the LM head needs
+// whole logits for the greedy argmax.
+//
+// Prologues.  Every CTA rebuilds the GEMV input vector x in shared memory:
+// RMSNorm(h) from the fp32 residual stream plus the previous phase's partials
+// (CTA 0 writes the updated residual back; two buffers alternate so no CTA
+// reads a vector while it is rewritten), or a copy of the bf16 attention
+// output / activation.  All cross-CTA data is read with ld.global.cg (L2), never
+// through the non-coherent L1.
+//
+// Attention (K4).  CTA (kv head g, split s) takes a contiguous page range of
+// the paged K/V cache for the G = H/KV query heads of g: q and the new k/v are
+// summed from the qkv partials (+bias, RoPE, bf16 rounding as the oracle),
+// the CTA owning the last page appends k/v to the pool, scores use 8 lanes per
+// position (16 dims each), an exp2 online softmax per head, and P.V with one
+// thread per (dim, 16-position group).  COMBINE merges the split partials
+// per head into the bf16 attention output.
+//
+// LM head (K5).  Each CTA keeps a (top-1, index, top-2) over its rows; after
+// the barrier every CTA merges the G partials (ties -> lower index), so all of
+// them agree on the token and on `done` without another barrier; CTA 0 writes
+// the token, margin and stop state exactly as select_token() does.
+#include "common.cuh"
+#include "kernels.h"
+#include "tma.cuh"
+
+namespace sr {
+
+constexpr int kMkWarps = 16;
+constexpr int kMkConsumers = kMkWarps * 32;
+constexpr int kMkThreads = kMkConsumers + 32;
+constexpr int kTR = 32;                    // tile rows
+constexpr int kTC = 256;                   // tile columns (bf16)
+constexpr int kTileBytes = kTR * kTC * 2;  // 16 KB
+#ifndef SR_MK_UPS
+#define SR_MK_UPS 2
+#endif
+constexpr int kUPS = SR_MK_UPS;            // tiles ("units") per ring stage
+constexpr int kStageBytes = kUPS * kTileBytes;
+constexpr int kMkMaxStages = 13;
+constexpr int kMkMaxGq = 8;
+constexpr int kMkProfEvents = SR_PROF_EVENTS;
+constexpr int kMkNorm = 5120 / kMkConsumers;
+constexpr int kMkAttnScratchFloats =
+    kMkMaxGq * 128 + kMkMaxGq * 64 + 3 * kMkMaxGq + 4 * kMkMaxGq * 128 + 2 * 128;
+constexpr int kMkTab = 256;  // max 32-row blocks of a tile-range phase (smem tables)
+
+enum { PH_QKV = 0, PH_O = 1, PH_GU = 2, PH_D = 3, PH_LM = 4 };
+
+struct Geo {
+  int tc, kt, nb, T, blockpart;  // tile columns (256, or K when K < 256), k tiles, row blocks, units
+};
+
+SR_DEV Geo mk_geo(const MkParams& p, int ph) {
+  int N, K;
+  switch (ph) {
+    case PH_QKV: N = p.qkv_rows; K = p.d; break;
+    case PH_O: N = p.d; K = p.q_dim; break;
+    case PH_GU: N = 2 * p.f; K = p.d; break;
+    case PH_D: N = p.d; K = p.f; break;
+    default: N = p.vocab_rows; K = p.d; break;
+  }
+  Geo g;
+  g.tc = K < kTC ? K : kTC;
+  g.kt = (K + g.tc - 1) / g.tc;
+  g.nb = (N + kTR - 1) / kTR;
+  g.T = g.nb * g.kt;
+  g.blockpart = (ph == PH_GU || ph == PH_LM);
+  return g;
+}
+
+SR_DEV void mk_range(const Geo& g, int c, int G, int& lo, int& hi) {
+  if (g.blockpart) {
+    lo = (int)((long long)g.nb * c / G) * g.kt;
+    hi = (int)((long long)g.nb * (c + 1) / G) * g.kt;
+  } else if (g.T >= G) {
+    lo = (int)((long long)g.T * c / G);
+    hi = (int)((long long)g.T * (c + 1) / G);
+  } else {  // fewer tiles than CTAs: one tile each for the first T CTAs
+    lo = c < g.T ? c : g.T;
+    hi = c < g.T ? c + 1 : g.T;
+  }
+}
+
+// this CTA's tile range of one phase, precomputed once per launch (no integer
+// division on the per-tile paths)
+struct PhaseInfo {
+  int lo, hi;    // unit range
+  int kt, tc;    // k tiles per row block, tile columns
+  int b0, k0;    // row block / k tile of unit lo
+  int bytes;     // bytes per tile
+  int pad;
+};
+
+SR_DEV PhaseInfo mk_phase_info(const MkParams& p, int ph, int c, int G) {
+  const Geo g = mk_geo(p, ph);
+  PhaseInfo pi;
+  mk_range(g, c, G, pi.lo, pi.hi);
+  pi.kt = g.kt;
+  pi.tc = g.tc;
+  pi.b0 = pi.lo / g.kt;
+  pi.k0 = pi.lo - pi.b0 * g.kt;
+  pi.bytes = kTR * g.tc * 2;
+  pi.pad = 0;
+  return pi;
+}
+
+// sum of the partials of `row` left by a tile-range phase, in CTA order
+// (deterministic).  tab[block] = {first contributing CTA, #contributors, slot j
+// of the block in the first CTA's range}; later contributors hold it at j = 0.
+// (packed in shared memory as c0 | n << 8 | j0 << 12)
+SR_DEV float mk_sum_parts(const float* part, const uint16_t* tab, int row, int maxj) {
+  const int b = row / kTR, r = row % kTR;
+  const int e = tab[b];
+  const int c0 = e & 0xff, n = (e >> 8) & 0xf, j0 = e >> 12;
+  const size_t cs = (size_t)maxj * kTR;
+  const float* q1 = part + (size_t)(c0 + 1) * cs + r;
+  // up to four contributors as independent predicated loads (all in flight
+  // together); more only for tiny models
+  const float a0 = __ldcg(part + (size_t)c0 * cs + (size_t)j0 * kTR + r);
+  const float a1 = n > 1 ? __ldcg(q1) : 0.f;
+  const float a2 = n > 2 ? __ldcg(q1 + cs) : 0.f;
+  const float a3 = n > 3 ? __ldcg(q1 + 2 * cs) : 0.f;
+  float s = ((a0 + a1) + a2) + a3;
+  if (n > 4) {
+    for (int q = 4; q < n; ++q) s += __ldcg(part + (size_t)(c0 + q) * cs + r);
+  }
+  return s;
+}
+
+SR_DEV void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(kMkConsumers) : "memory"); }
+
+SR_DEV float cblock_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) red[w] = v;
+  cbar();
+  float t = lane < kMkWarps ? red[lane] : 0.f;
+  t = warp_sum(t);
+  cbar();
+  return t;
+}
+
+SR_DEV uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// grid barrier over the consumer threads of all CTAs: the CTA barrier orders
+// every consumer's writes before thread 0's release-add; thread 0's acquire
+// poll + the CTA barrier order them before every consumer's later reads
+SR_DEV void mk_grid_sync(unsigned* ctr, unsigned& target, int G, int sleep_ns) {
+  cbar();
+  target += (unsigned)G;
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    const uint64_t t0 = global_ns();
+    for (unsigned spin = 0;; ++spin) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      if (sleep_ns > 0) __nanosleep(sleep_ns);
+      if ((spin & 1023) == 1023 && global_ns() - t0 > 5000000000ull) __trap();
+    }
+  }
+  cbar();
+}
+
+// x = bf16(h * rstd * w) with h = embedding row (mode 0) or hin + partials;
+// zero padding up to the next multiple of 256; CTA 0 stores h to hout
+SR_DEV void mk_norm_prologue(const MkParams& p, int mode, int tok, const float* hin,
+                             const float* part, const uint16_t* tab, const __nv_bfloat16* w,
+                             float* hout, __nv_bfloat16* xs, float* red, int c, int G) {
+  const int d = p.d, tid = threadIdx.x;
+  float hv[kMkNorm], wv[kMkNorm];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < kMkNorm; ++j) {
+    const int i = tid + j * kMkConsumers;
+    float v = 0.f, wj = 0.f;
+    if (i < d) {
+      wj = bf_to_f(w[i]);  // issued with the vector loads: one round trip in all
+      if (mode == 0)
+        v = bf_to_f(p.embed[(size_t)tok * d + i]);
+      else
+        v = __ldcg(hin + i) + mk_sum_parts(part, tab, i, p.maxj);
+    }
+    hv[j] = v;
+    wv[j] = wj;
+    ss += v * v;
+  }
+  ss = cblock_sum(ss, red);
+  const float rstd = rsqrtf(ss / d + p.eps);
+  const int dpad = (d + kTC - 1) / kTC * kTC;
+#pragma unroll
+  for (int j = 0; j < kMkNorm; ++j) {
+    const int i = tid + j * kMkConsumers;
+    if (i < d) {
+      xs[i] = __float2bfloat16_rn(hv[j] * rstd * wv[j]);
+      if (c == 0 && hout) hout[i] = hv[j];
+    }
+  }
+  for (int i = d + tid; i < dpad; i += kMkConsumers) xs[i] = __float2bfloat16_rn(0.f);
+  cbar();
+}
+
+SR_DEV void mk_stage_vec(const __nv_bfloat16* src, int K, __nv_bfloat16* xs) {
+  const int Kp = (K + kTC - 1) / kTC * kTC;
+  for (int i = threadIdx.x; i < K / 8; i += kMkConsumers) {
+    uint4 v = __ldcg(reinterpret_cast<const uint4*>(src) + i);
+    reinterpret_cast<uint4*>(xs)[i] = v;
+  }
+  for (int i = K + threadIdx.x; i < Kp; i += kMkConsumers) xs[i] = __float2bfloat16_rn(0.f);
+  cbar();
+}
+
+// ring position shared by the consumer warps (every warp walks every stage)
+struct RingPos {
+  int slot;
+  uint32_t par;
+  SR_DEV void advance(int S) {
+    if (++slot == S) {
+      slot = 0;
+      par ^= 1u;
+    }
+  }
+};
+
+// consume this CTA's tiles of one GEMV phase (same order as the producer):
+// a ring stage carries up to kUPS consecutive tiles of the phase, so the
+// per-stage handshake (wait, arrive) is paid once per kUPS x 16 KB
+template <int PH>
+SR_DEV void mk_gemv(const MkParams& p, const PhaseInfo& pi, int c, const uint8_t* ring,
+                    uint64_t* full, uint64_t* empty, const __nv_bfloat16* xs, RingPos& rp, int S,
+                    Top2& best) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lo = pi.lo, hi = pi.hi, kt = pi.kt, tc = pi.tc;
+  const int row_bytes = tc * 2;
+  const bool active = lane * 8 < tc;
+  int b = pi.b0, k = pi.k0;
+  float a0 = 0.f, a1 = 0.f;
+  for (int u0 = lo; u0 < hi; u0 += kUPS) {
+    mbar_wait(&full[rp.slot], rp.par);
+    const uint8_t* stage = ring + (size_t)rp.slot * kStageBytes;
+    const int nu = hi - u0 < kUPS ? hi - u0 : kUPS;
+#pragma unroll
+    for (int q = 0; q < kUPS; ++q) {
+      if (q < nu) {
+        const int u = u0 + q;
+        if (active) {
+          const uint8_t* tile = stage + q * kTileBytes;
+          const uint4 w0 = *reinterpret_cast<const uint4*>(tile + warp * row_bytes + lane * 16);
+          const uint4 w1 = *reinterpret_cast<const uint4*>(tile + (warp + 16) * row_bytes + lane * 16);
+          const uint4 xv = *reinterpret_cast<const uint4*>(xs + k * tc + lane * 8);
+          a0 = dot8(w0, xv, a0);
+          a1 = dot8(w1, xv, a1);
+        }
+        if (q == nu - 1) {  // stage fully read: hand it back to the producer
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[rp.slot]);
+          rp.advance(S);
+        }
+        if (k == kt - 1 || u == hi - 1) {
+          a0 = warp_sum(a0);
+          a1 = warp_sum(a1);
+          if (lane == 0) {
+            if constexpr (PH == PH_QKV || PH == PH_O || PH == PH_D) {
+              float* part = PH == PH_QKV ? p.part_qkv : PH == PH_O ? p.part_o : p.part_d;
+              float* dst = part + ((size_t)c * p.maxj + (b - pi.b0)) * kTR;
+              dst[warp] = a0;
+              dst[warp + 16] = a1;
+            } else if constexpr (PH == PH_GU) {
+              p.act[b * 16 + warp] = __float2bfloat16_rn(a0 / (1.f + __expf(-a0)) * a1);
+            } else {
+              const int r0 = b * kTR + warp;
+              if (r0 < p.vocab_text) best.push(a0, r0);
+              if (r0 + 16 < p.vocab_text) best.push(a1, r0 + 16);
+            }
+          }
+          a0 = a1 = 0.f;
+        }
+        if (++k == kt) {
+          k = 0;
+          ++b;
+        }
+      }
+    }
+  }
+}
+
+SR_DEV float mk_qkv_val(const MkParams& p, const __nv_bfloat16* bias, const uint16_t* tab,
+                        int row) {
+  return mk_sum_parts(p.part_qkv, tab, row, p.maxj) + bf_to_f(bias[row]);
+}
+
+// K/V of one page held in registers: 8 lanes per position x 16 dims of K
+// (scores), one thread per (dim, 16-position group) of V (P.V)
+struct PageRegs {
+  uint4 k0, k1;
+  __nv_bfloat16 v[16];
+};
+
+SR_DEV void mk_load_page(const MkParams& p, int layer, int g, int page, int nval, int posl,
+                         int sub, int dd, int grp, PageRegs& r) {
+  if (posl < nval) {
+    const uint4* kr = reinterpret_cast<const uint4*>(
+        p.k_pool + kv_offset(layer, page, g, posl, p.n_pages, p.KV) + sub * 16);
+    r.k0 = __ldcg(kr);
+    r.k1 = __ldcg(kr + 1);
+  }
+  const __nv_bfloat16* vb = p.v_pool + kv_offset(layer, page, g, 0, p.n_pages, p.KV) + dd;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int pl = grp * 16 + q;
+    if (pl < nval) r.v[q] = __ldcg(vb + (size_t)pl * kHeadDim);
+  }
+}
+
+// Attention of kv head g over pages [p0, p1) for its Gq query heads; the split
+// partials (m, l, O) go to apart, and the last split CTA of g to finish (atomic
+// ticket) merges all splits of g into the bf16 attention output.
+SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_table,
+                         const __nv_bfloat16* bias, const uint16_t* tab, int c, int S_a,
+                         int npages, float* sm, int* s_flag) {
+  const int Gq = p.H / p.KV;
+  const int g = c / S_a, s = c % S_a;
+  if (g >= p.KV) return;  // uniform per CTA
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int p0 = (int)((long long)npages * s / S_a), p1 = (int)((long long)npages * (s + 1) / S_a);
+  float* qs = sm;                              // [8][128]
+  float* ps = qs + kMkMaxGq * 128;             // [8][64]
+  float* alph = ps + kMkMaxGq * 64;            // [8]
+  float* mrun = alph + kMkMaxGq;               // [8]
+  float* lrun = mrun + kMkMaxGq;               // [8]
+  float* red = lrun + kMkMaxGq;                // [4][8][128]
+  float* kn = red + 4 * kMkMaxGq * 128;        // [128] new k (rotated, bf16 values)
+  float* vn = kn + 128;                        // [128] new v
+  const float scale = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
+  const int posl = warp * 4 + (lane >> 3), sub = lane & 7;
+  const int dd = tid % kHeadDim, grp = tid / kHeadDim;
+
+  // first page's K/V loads go out before anything else (independent of q)
+  PageRegs cur;
+  {
+    const int nval = min(kPage, pos + 1 - p0 * kPage);
+    mk_load_page(p, layer, g, page_table[p0], nval, posl, sub, dd, grp, cur);
+  }
+  for (int t = tid; t < Gq * kHalf; t += kMkConsumers) {
+    const int j = t / kHalf, i = t % kHalf;
+    const int r0 = (g * Gq + j) * kHeadDim + i;
+    const float v0 = mk_qkv_val(p, bias, tab, r0), v1 = mk_qkv_val(p, bias, tab, r0 + kHalf);
+    const float cs = p.rope[((size_t)pos * kHalf + i) * 2], sn = p.rope[((size_t)pos * kHalf + i) * 2 + 1];
+    qs[j * 128 + i] = round_bf16(v0 * cs - v1 * sn);
+    qs[j * 128 + i + kHalf] = round_bf16(v1 * cs + v0 * sn);
+  }
+  const bool has_new = p1 == npages;
+  if (has_new) {  // new position: k / v from the partials; appended to the pool
+    const int page = page_table[pos / kPage];
+    const size_t base = kv_offset(layer, page, g, pos % kPage, p.n_pages, p.KV);
+    if (tid < kHalf) {
+      const int r0 = p.q_dim + g * kHeadDim + tid;
+      const float v0 = mk_qkv_val(p, bias, tab, r0), v1 = mk_qkv_val(p, bias, tab, r0 + kHalf);
+      const float cs = p.rope[((size_t)pos * kHalf + tid) * 2];
+      const float sn = p.rope[((size_t)pos * kHalf + tid) * 2 + 1];
+      const __nv_bfloat16 y0 = __float2bfloat16_rn(v0 * cs - v1 * sn);
+      const __nv_bfloat16 y1 = __float2bfloat16_rn(v1 * cs + v0 * sn);
+      p.k_pool[base + tid] = y0;
+      p.k_pool[base + tid + kHalf] = y1;
+      kn[tid] = bf_to_f(y0);
+      kn[tid + kHalf] = bf_to_f(y1);
+    } else if (tid < kHalf + kHeadDim) {
+      const int d2 = tid - kHalf;
+      const int r = p.q_dim + p.kv_dim + g * kHeadDim + d2;
+      const __nv_bfloat16 y = __float2bfloat16_rn(mk_qkv_val(p, bias, tab, r));
+      p.v_pool[base + d2] = y;
+      vn[d2] = bf_to_f(y);
+    }
+  }
+  if (tid < kMkMaxGq) {
+    mrun[tid] = -INFINITY;
+    lrun[tid] = 0.f;
+  }
+  float acc[kMkMaxGq];
+#pragma unroll
+  for (int j = 0; j < kMkMaxGq; ++j) acc[j] = 0.f;
+  cbar();
+
+  for (int pg_i = p0; pg_i < p1; ++pg_i) {
+    const int P0 = pg_i * kPage;
+    const int nval = min(kPage, pos + 1 - P0);
+    const int newl = has_new && pg_i == p1 - 1 ? pos - P0 : -1;  // slot of the new position
+    // scores: 8 lanes per position, 16 dims per lane
+    {
+      float sc[kMkMaxGq];
+#pragma unroll
+      for (int j = 0; j < kMkMaxGq; ++j) sc[j] = 0.f;
+      if (posl < nval) {
+        float kf[16];
+        if (posl == newl) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) kf[e] = kn[sub * 16 + e];
+        } else {
+          const uint32_t kw[8] = {cur.k0.x, cur.k0.y, cur.k0.z, cur.k0.w,
+                                  cur.k1.x, cur.k1.y, cur.k1.z, cur.k1.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float2 f2 = bf2_to_f2(kw[e]);
+            kf[2 * e] = f2.x;
+            kf[2 * e + 1] = f2.y;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kMkMaxGq; ++j) {
+          if (j < Gq) {
+            const float* q = qs + j * 128 + sub * 16;
+            float a = 0.f;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) a = fmaf(q[e], kf[e], a);
+            sc[j] = a;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kMkMaxGq; ++j) {
+        if (j < Gq) {
+          float a = sc[j];
+          a += __shfl_xor_sync(0xffffffffu, a, 1);
+          a += __shfl_xor_sync(0xffffffffu, a, 2);
+          a += __shfl_xor_sync(0xffffffffu, a, 4);
+          if (sub == 0) ps[j * 64 + posl] = posl < nval ? a * scale : -INFINITY;
+        }
+      }
+    }
+    cbar();
+    if (warp < Gq) {  // online softmax of head `warp` over this page
+      const int j = warp;
+      const float s0 = ps[j * 64 + lane], s1 = ps[j * 64 + lane + 32];
+      const float mx = warp_max(fmaxf(s0, s1));
+      const float m_old = mrun[j];
+      const float m_new = fmaxf(m_old, mx);
+      const float e0 = exp2f(s0 - m_new), e1 = exp2f(s1 - m_new);
+      const float sum = warp_sum(e0 + e1);
+      ps[j * 64 + lane] = e0;
+      ps[j * 64 + lane + 32] = e1;
+      __syncwarp();
+      if (lane == 0) {
+        const float a = exp2f(m_old - m_new);
+        alph[j] = a;
+        lrun[j] = lrun[j] * a + sum;
+        mrun[j] = m_new;
+      }
+    }
+    cbar();
+    {
+      float vf[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) vf[q] = bf_to_f(cur.v[q]);
+      if (newl >= grp * 16 && newl < grp * 16 + 16) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (grp * 16 + q == newl) vf[q] = vn[dd];
+      }
+      if (pg_i + 1 < p1) {  // next page's loads overlap this page's P.V
+        const int nv2 = min(kPage, pos + 1 - (pg_i + 1) * kPage);
+        mk_load_page(p, layer, g, page_table[pg_i + 1], nv2, posl, sub, dd, grp, cur);
+      }
+#pragma unroll
+      for (int j = 0; j < kMkMaxGq; ++j)
+        if (j < Gq) acc[j] *= alph[j];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int pl = grp * 16 + q;
+        if (pl < nval) {
+#pragma unroll
+          for (int j = 0; j < kMkMaxGq; ++j)
+            if (j < Gq) acc[j] = fmaf(ps[j * 64 + pl], vf[q], acc[j]);
+        }
+      }
+    }
+    cbar();
+  }
+#pragma unroll
+  for (int j = 0; j < kMkMaxGq; ++j)
+    if (j < Gq) red[(grp * kMkMaxGq + j) * 128 + dd] = acc[j];
+  cbar();
+  if (grp == 0) {
+    for (int j = 0; j < Gq; ++j) {
+      const float o = red[(0 * kMkMaxGq + j) * 128 + dd] + red[(1 * kMkMaxGq + j) * 128 + dd] +
+                      red[(2 * kMkMaxGq + j) * 128 + dd] + red[(3 * kMkMaxGq + j) * 128 + dd];
+      p.apart[((size_t)c * kMkMaxGq + j) * 130 + dd] = o;
+    }
+  }
+  if (tid < Gq) {
+    p.apart[((size_t)c * kMkMaxGq + tid) * 130 + 128] = mrun[tid];
+    p.apart[((size_t)c * kMkMaxGq + tid) * 130 + 129] = lrun[tid];
+  }
+  // last split of kv head g merges the splits (classic last-block pattern)
+  cbar();
+  if (tid == 0) {
+    __threadfence();
+    const int ticket = atomicAdd(p.attn_cnt + g, 1);
+    const int last = ticket == S_a - 1;
+    if (last) p.attn_cnt[g] = 0;  // re-armed for the next layer (after a grid barrier)
+    __threadfence();
+    *s_flag = last;
+  }
+  cbar();
+  if (!*s_flag) return;
+  // merge: (m, l) of every split and head into shared memory, per-head
+  // weights exp2(m_s - M) / L, then one weighted sum per output element
+  float* ml = sm;                      // [S_a][Gq][2] (reuses qs / ps)
+  float* wts = red;                    // [S_a][Gq]
+  for (int t = tid; t < S_a * Gq; t += kMkConsumers) {
+    const int q = t / Gq, j = t - q * Gq;
+    const float* a = p.apart + ((size_t)(g * S_a + q) * kMkMaxGq + j) * 130;
+    ml[2 * t] = __ldcg(a + 128);
+    ml[2 * t + 1] = __ldcg(a + 129);
+  }
+  cbar();
+  if (warp < Gq) {
+    const int j = warp;
+    float M = -INFINITY;
+    for (int q = lane; q < S_a; q += 32) M = fmaxf(M, ml[2 * (q * Gq + j)]);
+    M = warp_max(M);
+    float Ls = 0.f;
+    for (int q = lane; q < S_a; q += 32) {
+      const float w = exp2f(ml[2 * (q * Gq + j)] - M);
+      wts[q * Gq + j] = w;
+      Ls += w * ml[2 * (q * Gq + j) + 1];
+    }
+    Ls = warp_sum(Ls);
+    __syncwarp();
+    const float inv = 1.f / Ls;
+    for (int q = lane; q < S_a; q += 32) wts[q * Gq + j] *= inv;
+  }
+  cbar();
+  for (int o = tid; o < Gq * kHeadDim; o += kMkConsumers) {
+    const int j = o / kHeadDim, d2 = o - j * kHeadDim;
+    const float* a = p.apart + ((size_t)(g * S_a) * kMkMaxGq + j) * 130 + d2;
+    float acc_o = 0.f;
+#pragma unroll 16
+    for (int q = 0; q < S_a; ++q)
+      acc_o = fmaf(wts[q * Gq + j], __ldcg(a + (size_t)q * kMkMaxGq * 130), acc_o);
+    p.attn[(size_t)(g * Gq + j) * kHeadDim + d2] = __float2bfloat16_rn(acc_o);
+  }
+}
+
+// Walks this CTA's tile sequence: per token, layer 0..L-1 x (qkv, o, gate/up,
+// down), then the LM head; wraps to the next token.  Empty phases are skipped.
+struct MkCursor {
+  int l, k, u, hi, kk, bb, kt, tc, bytes;
+  const CUtensorMap* map;
+  SR_DEV void enter(const MkParams& p, const PhaseInfo* ph) {
+    for (;;) {
+      const PhaseInfo& pi = ph[l < p.L ? k : PH_LM];
+      map = p.maps + (l < p.L ? l * 4 + k : p.L * 4);
+      u = pi.lo;
+      hi = pi.hi;
+      kk = pi.k0;
+      bb = pi.b0;
+      kt = pi.kt;
+      tc = pi.tc;
+      bytes = pi.bytes;
+      if (u < hi) return;
+      step_phase(p);
+    }
+  }
+  SR_DEV void step_phase(const MkParams& p) {
+    if (l < p.L && ++k < 4) return;
+    k = 0;
+    if (++l > p.L) l = 0;
+  }
+  SR_DEV void init(const MkParams& p, const PhaseInfo* ph) {
+    l = 0;
+    k = 0;
+    enter(p, ph);
+  }
+  SR_DEV void next(const MkParams& p, const PhaseInfo* ph) {
+    if (++kk == kt) {
+      kk = 0;
+      ++bb;
+    }
+    if (++u < hi) return;
+    step_phase(p);
+    enter(p, ph);
+  }
+  SR_DEV int col() const { return kk * tc; }
+  SR_DEV int row() const { return bb * kTR; }
+};
+
+__global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams p) {
+  extern __shared__ __align__(1024) uint8_t mk_smem[];
+  __shared__ __align__(8) uint64_t full[kMkMaxStages];
+  __shared__ __align__(8) uint64_t empty[kMkMaxStages];
+  __shared__ float red[32];
+  __shared__ float s_v1[kMkWarps], s_v2[kMkWarps];
+  __shared__ int s_i1[kMkWarps];
+  __shared__ int s_tok;
+  __shared__ int s_flag;
+  __shared__ uint16_t s_tab[3][kMkTab];  // contributor tables: qkv, o, down
+  __shared__ PhaseInfo s_ph[5];
+  __shared__ float s_margin;
+  __shared__ volatile int s_stop;
+
+  const int S = p.stages;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = mk_smem;
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(mk_smem + (size_t)S * kStageBytes);
+  float* scratch = reinterpret_cast<float*>(xs);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kMkWarps);
+    }
+    s_stop = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 5) s_ph[threadIdx.x] = mk_phase_info(p, threadIdx.x, blockIdx.x, gridDim.x);
+  __syncthreads();
+
+  DecodeState* st = p.st;
+  const int L = p.L;
+
+  if (warp == kMkWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      // a CTA with no tiles in any phase (tiny models) has nothing to stream
+      int mine = 0;
+      for (int ph = 0; ph <= PH_LM; ++ph) mine += s_ph[ph].hi - s_ph[ph].lo;
+      uint32_t n = 0;
+      if (mine > 0) {
+        MkCursor ld, pf;
+        ld.init(p, s_ph);
+        pf.init(p, s_ph);
+        uint32_t npf = 0, nld = 0;  // units prefetched into L2 / loaded
+        const uint32_t ahead = (uint32_t)(S * kUPS + (p.l2_ahead > 0 ? p.l2_ahead : 0));
+        int slot = 0;
+        uint32_t par = 1u;
+        const uint64_t pol = l2_policy_evict_first();
+        for (;;) {
+          // L2 prefetch run-ahead: HBM keeps streaming while the consumers sit
+          // in latency-bound phases longer than the shared-memory ring covers
+          if (p.l2_ahead >= 0) {
+            while (npf < nld + ahead) {
+              tma_prefetch_2d(pf.map, pf.col(), pf.row());
+              pf.next(p, s_ph);
+              ++npf;
+            }
+          }
+          bool stop = false;
+          while (!mbar_try(&empty[slot], par)) {
+            if (s_stop) {
+              stop = true;
+              break;
+            }
+          }
+          if (stop || s_stop) break;
+          if (p.trace) p.trace[c * 8 + 3] = (int)n;
+          {
+            const int nu = ld.hi - ld.u < kUPS ? ld.hi - ld.u : kUPS;
+            mbar_expect_tx(&full[slot], nu * ld.bytes);
+            uint8_t* dst = ring + (size_t)slot * kStageBytes;
+            for (int q = 0; q < nu; ++q) {
+              if (p.evict_first)
+                tma_load_2d_hint(dst + q * kTileBytes, ld.map, &full[slot], ld.col(), ld.row(), pol);
+              else
+                tma_load_2d(dst + q * kTileBytes, ld.map, &full[slot], ld.col(), ld.row());
+              ld.next(p, s_ph);
+            }
+            nld += nu;
+          }
+          ++n;
+          if (++slot == S) {
+            slot = 0;
+            par ^= 1u;
+          }
+        }
+      }
+      // let every issued copy land before the CTA exits
+      for (uint32_t m = n > (uint32_t)S ? n - (uint32_t)S : 0u; m < n; ++m)
+        mbar_wait(&full[m % (uint32_t)S], (m / (uint32_t)S) & 1u);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  for (int i = threadIdx.x; i < 3 * kMkTab; i += kMkConsumers) (&s_tab[0][0])[i] = p.ctab[i];
+  cbar();
+  int pos = st->pos, tok = st->token, n_gen = st->n_gen;
+  const int max_new = st->max_new;
+  const int* page_table = st->page_table;
+  const uint8_t* token_class = st->token_class;
+  unsigned* bar = &st->bar;
+  unsigned target = 0;
+  RingPos rp{0, 0u};
+  const int Gq = p.H / p.KV;
+  (void)Gq;
+  bool done = st->done != 0;
+  // SR_MK_PROF: CTA 0 records a globaltimer stamp after every step of the
+  // first decoded token (sr_debug_profile)
+  const bool prof = p.prof != nullptr && c == 0 && threadIdx.x == 0;
+  int ev = 0;
+  int tstep = 0;
+#define MK_EV()                                                                        \
+  do {                                                                                 \
+    if (prof && ev < kMkProfEvents) p.prof[ev++] = global_ns();                        \
+    if (p.trace && threadIdx.x == 0) {                                                 \
+      volatile int* tr = p.trace + c * 8;                                              \
+      tr[0] = ++tstep;                                                                 \
+      tr[1] = rp.slot;                                                                 \
+      tr[2] = (int)target;                                                             \
+      tr[4] = n_gen;                                                                   \
+    }                                                                                  \
+  } while (0)
+
+  while (!done) {
+    MK_EV();
+    const int npages = pos / kPage + 1;
+    // splits per kv head: every CTA busy at long context, >= 2 pages per split
+    int S_a = G / p.KV;
+    if (S_a > (npages + 1) / 2) S_a = (npages + 1) / 2;
+    if (S_a < 1) S_a = 1;
+    Top2 best;
+    best.init();
+    for (int l = 0; l < L; ++l) {
+      const MkLayer ly = p.layers[l];
+      // QKV
+      if (l == 0)
+        mk_norm_prologue(p, 0, tok, nullptr, nullptr, s_tab[2], ly.ln1, p.hA, xs, red, c, G);
+      else
+        mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], ly.ln1, p.hA, xs, red, c, G);
+      MK_EV();  // 1 qkv prologue
+      mk_gemv<PH_QKV>(p, s_ph[PH_QKV], c, ring, full, empty, xs, rp, S, best);
+      MK_EV();  // 2 qkv gemv
+      mk_grid_sync(bar, target, G, p.bar_sleep);
+      MK_EV();  // 3 sync
+      // attention (+ merge of the splits by the last split CTA of each kv head)
+      mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, npages, scratch, &s_flag);
+      MK_EV();  // 4 attention
+      mk_grid_sync(bar, target, G, p.bar_sleep);
+      MK_EV();  // 5 sync
+      // O
+      mk_stage_vec(p.attn, p.q_dim, xs);
+      MK_EV();  // 8 stage
+      mk_gemv<PH_O>(p, s_ph[PH_O], c, ring, full, empty, xs, rp, S, best);
+      MK_EV();  // 9 o gemv
+      mk_grid_sync(bar, target, G, p.bar_sleep);
+      MK_EV();  // 10 sync
+      // gate / up
+      mk_norm_prologue(p, 1, tok, p.hA, p.part_o, s_tab[1], ly.ln2, p.hB, xs, red, c, G);
+      MK_EV();  // 11 prologue
+      mk_gemv<PH_GU>(p, s_ph[PH_GU], c, ring, full, empty, xs, rp, S, best);
+      MK_EV();  // 12 gu gemv
+      mk_grid_sync(bar, target, G, p.bar_sleep);
+      MK_EV();  // 13 sync
+      // down
+      mk_stage_vec(p.act, p.f, xs);
+      MK_EV();  // 14 stage
+      mk_gemv<PH_D>(p, s_ph[PH_D], c, ring, full, empty, xs, rp, S, best);
+      MK_EV();  // 15 down gemv
+      mk_grid_sync(bar, target, G, p.bar_sleep);
+      MK_EV();  // 16 sync
+    }
+    // LM head + greedy argmax
+    mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], p.ln_f, nullptr, xs, red, c, G);
+    MK_EV();
+    mk_gemv<PH_LM>(p, s_ph[PH_LM], c, ring, full, empty, xs, rp, S, best);
+    MK_EV();
+    if (lane == 0) {
+      s_v1[warp] = best.v1;
+      s_v2[warp] = best.v2;
+      s_i1[warp] = best.i1;
+    }
+    cbar();
+    if (threadIdx.x == 0) {
+      Top2 b;
+      b.init();
+      for (int w = 0; w < kMkWarps; ++w) b.merge(s_v1[w], s_i1[w], s_v2[w]);
+      p.lm_part[c * 3 + 0] = b.v1;
+      p.lm_part[c * 3 + 1] = b.v2;
+      p.lm_part[c * 3 + 2] = __int_as_float(b.i1);
+    }
+    mk_grid_sync(bar, target, G, p.bar_sleep);
+    MK_EV();
+    if (warp == 0) {
+      Top2 b;
+      b.init();
+      for (int i = lane; i < G; i += 32)
+        b.merge(__ldcg(p.lm_part + i * 3), __float_as_int(__ldcg(p.lm_part + i * 3 + 2)),
+                __ldcg(p.lm_part + i * 3 + 1));
+      warp_top2(b);
+      if (lane == 0) {
+        s_tok = b.i1;
+        s_margin = b.v1 - b.v2;
+      }
+    }
+    cbar();
+    const int t = s_tok;
+    const int cls = token_class[t];
+    int finish = SR_FINISH_LENGTH;
+    done = false;
+    if (cls == SR_CLASS_END_THINK) {
+      done = true;
+      finish = SR_FINISH_END_THINK;
+    } else if (cls == SR_CLASS_STOP) {
+      done = true;
+      finish = SR_FINISH_STOP;
+    } else if (n_gen + 1 >= max_new) {
+      done = true;
+    }
+    if (c == 0 && threadIdx.x == 0) {
+      st->out_ids[n_gen] = t;
+      if (st->margins) st->margins[n_gen] = s_margin;
+      st->n_gen = n_gen + 1;
+      st->done = done ? 1 : 0;
+      st->finish = finish;
+      if (!done) {
+        st->token = t;
+        st->pos = pos + 1;
+        st->ctx_len = pos + 2;
+      }
+      st->out_hdr[0] = n_gen + 1;
+      st->out_hdr[1] = finish;
+    }
+    n_gen += 1;
+    tok = t;
+    pos += 1;
+    MK_EV();
+    if (prof) ev = kMkProfEvents;  // first token only
+  }
+#undef MK_EV
+  if (threadIdx.x == 0) s_stop = 1;
+}
+
+// ------------------------------------------------------------------- host ---
+size_t mk_smem_bytes(int stages, int xs_elems) {
+  size_t xs = (size_t)xs_elems * 2;
+  const size_t attn = (size_t)kMkAttnScratchFloats * 4;
+  if (xs < attn) xs = attn;
+  return (size_t)stages * kStageBytes + xs;
+}
+
+int mk_pick_stages(int xs_elems) {
+  int s = kMkMaxStages;
+  while (s > 2 && mk_smem_bytes(s, xs_elems) > 225 * 1024) --s;
+  return s;
+}
+
+int mk_max_j(int N, int K, int num_sms) {
+  const int kt = (K + kTC - 1) / kTC, nb = (N + kTR - 1) / kTR;
+  const int T = nb * kt;
+  const int per = (T + num_sms - 1) / num_sms;
+  return per > 0 ? (per - 1) / kt + 2 : 1;
+}
+
+int mk_tile_rows() { return kTR; }
+int mk_tile_cols() { return kTC; }
+
+cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream) {
+  const size_t smem = mk_smem_bytes(p.stages, p.xs_elems);
+  static size_t attr = 0;
+  if (attr < smem) {
+    cudaError_t e =
+        cudaFuncSetAttribute(decode_mk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms);
+  cfg.blockDim = dim3(kMkThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_mk_kernel, p);
+}
+
+}  // namespace sr

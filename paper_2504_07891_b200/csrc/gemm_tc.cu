@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace sr {
 
@@ -24,43 +25,6 @@ constexpr int kTcThreads = 128;
 constexpr int kBK = 64;                 // k-block: 64 bf16 = one 128-B swizzle row
 constexpr int kWRows = 128;             // UMMA_M
 constexpr int kWStageBytes = kWRows * kBK * 2;  // 16 KB
-
-SR_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-SR_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-SR_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
-SR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  for (uint32_t spin = 0;; ++spin) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if (spin > (1u << 26)) __trap();
-  }
-}
-
-SR_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
 
 // UMMA shared-memory descriptor: K-major, 128-B swizzle, 8-row groups 1024 B apart
 SR_DEV uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -248,19 +212,25 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D bf16 row-major [rows, cols] tensor map with a (64 x box_rows) 128-B swizzled box
-int make_tmap_bf16(void* out_map, const void* ptr, int rows, int cols, int box_rows) {
+// 2-D bf16 row-major [rows, cols] tensor map with a (box_cols x box_rows) box,
+// 128-B swizzled (the GEMM's K-major operand tiles) or plain row-major
+int make_tmap_bf16_box(void* out_map, const void* ptr, int rows, int cols, int box_cols,
+                       int box_rows, bool swizzle128) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return -1;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn((CUtensorMap*)out_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr),
                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+int make_tmap_bf16(void* out_map, const void* ptr, int rows, int cols, int box_rows) {
+  return make_tmap_bf16_box(out_map, ptr, rows, cols, kBK, box_rows, true);
 }
 
 int tc_token_tile(int M) {

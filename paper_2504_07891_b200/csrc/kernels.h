@@ -1,6 +1,8 @@
 // Kernel parameter blocks and host launchers shared by the runtime.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace sr {
@@ -121,6 +123,8 @@ struct TcGemmArgs {
   int M, N, K, splits;
 };
 int make_tmap_bf16(void* out_map, const void* ptr, int rows, int cols, int box_rows);
+int make_tmap_bf16_box(void* out_map, const void* ptr, int rows, int cols, int box_cols,
+                       int box_rows, bool swizzle128);
 int tc_token_tile(int M);
 int tc_pick_splits(int M, int N, int K, int num_sms);
 cudaError_t gemm_tc_launch(const TcGemmArgs& a, cudaStream_t stream);
@@ -165,6 +169,53 @@ struct ReadoutParams {
   sr_readout* out;
 };
 cudaError_t readout_launch(const ReadoutParams& p, int num_sms, cudaStream_t stream);
+
+// persistent weight-streaming decode kernel (decode_mk.cu)
+#define SR_PROF_EVENTS 2048
+struct MkLayer {
+  const __nv_bfloat16* ln1;
+  const __nv_bfloat16* bqkv;
+  const __nv_bfloat16* ln2;
+  const void* pad;
+};
+
+struct MkParams {
+  const CUtensorMap* maps;   // device [L*4 + 1]: per layer qkv, o, gate/up, down; then LM head
+  const MkLayer* layers;     // device [L]
+  const __nv_bfloat16* embed;
+  const __nv_bfloat16* ln_f;
+  const float* rope;
+  __nv_bfloat16* k_pool;
+  __nv_bfloat16* v_pool;
+  float* hA;                 // residual stream, two alternating buffers [d]
+  float* hB;
+  const uint16_t* ctab;      // [3][256] per 32-row block of qkv / o / down: first CTA |
+                             // #contributors << 8 | slot << 12 (host-built)
+  int* attn_cnt;             // [KV] split tickets of the attention merge
+  float* part_qkv;           // [G][maxj][32] split-row partials
+  float* part_o;
+  float* part_d;
+  float* apart;              // [G][8][130] attention split partials
+  float* lm_part;            // [G][3] per-CTA (top1, top2, index)
+  __nv_bfloat16* act;        // [f]
+  __nv_bfloat16* attn;       // [q_dim]
+  DecodeState* st;
+  volatile int* trace;       // SR_MK_TRACE: mapped host [G][8] progress words, or null
+  unsigned long long* prof;  // SR_MK_PROF: [SR_PROF_EVENTS] globaltimer stamps, or null
+  int L, d, H, KV, f, vocab_rows, vocab_text, n_pages, q_dim, kv_dim, qkv_rows;
+  float eps;
+  int maxj, stages, xs_elems;
+  int l2_ahead;              // tiles prefetched into L2 beyond the shared-memory ring
+  int bar_sleep;             // ns of backoff between grid-barrier polls
+  int evict_first;           // stream weights with an L2 evict-first policy
+};
+
+size_t mk_smem_bytes(int stages, int xs_elems);
+int mk_pick_stages(int xs_elems);
+int mk_max_j(int N, int K, int num_sms);
+int mk_tile_rows();
+int mk_tile_cols();
+cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream);
 
 // decode-loop bookkeeping kernels
 cudaError_t decode_begin_launch(DecodeState* st, const DecodeState* h_init, cudaStream_t stream);

@@ -44,7 +44,8 @@ constexpr int kAttnPrefillSplit = 16;
 
 struct Layout {  // workspace carve-up (byte offsets)
   size_t st, h, x, q, attn, act, part, apart, actr, lm_v1, lm_v2, lm_i1, lm_ctr, logits, ro_cnt,
-      total;
+      mk_maps, mk_layers, mk_h, mk_part, mk_apart, mk_lm, mk_prof, mk_ctab, total;
+  int mk_maxj;
   int nsplit_decode;
   size_t part_floats;
 };
@@ -78,6 +79,18 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
   L.lm_ctr = take(64);
   L.logits = take((size_t)d.vocab_rows * 4);
   L.ro_cnt = take(64);
+  // persistent decode kernel (decode_mk.cu)
+  const int qd_i = d.n_heads * SR_HEAD_DIM, qkv_i = qd_i + 2 * d.n_kv_heads * SR_HEAD_DIM;
+  L.mk_maxj = std::max({mk_max_j(qkv_i, d.d_model, num_sms), mk_max_j(d.d_model, qd_i, num_sms),
+                        mk_max_j(d.d_model, d.d_ffn, num_sms)});
+  L.mk_maps = take(((size_t)d.n_layers * 4 + 1) * sizeof(CUtensorMap));
+  L.mk_layers = take((size_t)d.n_layers * sizeof(MkLayer));
+  L.mk_h = take(2 * (size_t)d.d_model * 4);
+  L.mk_part = take(3 * (size_t)num_sms * L.mk_maxj * mk_tile_rows() * 4);
+  L.mk_apart = take((size_t)num_sms * 8 * 130 * 4);
+  L.mk_lm = take((size_t)num_sms * 3 * 4);
+  L.mk_prof = take((size_t)SR_PROF_EVENTS * 8);
+  L.mk_ctab = take(3 * 256 * 2 + 64 * 4);
   L.total = o;
   return L;
 }
@@ -107,6 +120,9 @@ struct Model {
   bool pdl = true;
   bool use_tc = true;  // tcgen05 GEMM (K6); SR_GEMM=mma selects the mma.sync reference
   bool stream_decode = false;  // SR_DECODE=stream: per-token host loop (profiling only)
+  bool graph_decode = false;   // SR_DECODE=graph: per-kernel decode graph (A/B reference)
+  MkParams mk{};
+  int* trace_host = nullptr;
   bool attn_simt = false;      // SR_ATTN=simt: CUDA-core split-KV attention (A/B reference)
   bool prefetch = false;       // SR_PREFETCH=1: GEMV L2 prefetch before the PDL wait
   struct alignas(64) TMap { CUtensorMap m; };
@@ -133,6 +149,112 @@ struct Model {
       for (int t = 0; t < 4; ++t)
         if (make_tmap_bf16(&amaps[i][t].m, a[i], d.max_tokens, acols[i], tiles[t]))
           return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for an activation");
+    return 0;
+  }
+
+  // tensor maps (32-row x 256-col boxes, no swizzle) + per-layer table for the
+  // persistent decode kernel, written into the workspace once
+  int build_mk() {
+    const int n = d.n_layers * 4 + 1;
+    std::vector<TMap> maps(n);
+    for (int l = 0; l < d.n_layers; ++l) {
+      const void* w[4] = {lw(l, WQKV), lw(l, WO), lw(l, WGU), lw(l, WD)};
+      const int rows[4] = {qkv_rows, d.d_model, 2 * d.d_ffn, d.d_model};
+      const int cols[4] = {d.d_model, q_dim, d.d_model, d.d_ffn};
+      for (int i = 0; i < 4; ++i)
+        if (make_tmap_bf16_box(&maps[l * 4 + i].m, w[i], rows[i], cols[i],
+                               std::min(cols[i], mk_tile_cols()), mk_tile_rows(), false))
+          return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for a decode weight map");
+    }
+    if (make_tmap_bf16_box(&maps[n - 1].m, lm_head, d.vocab_rows, d.d_model,
+                           std::min(d.d_model, mk_tile_cols()), mk_tile_rows(), false))
+      return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for the LM-head map");
+    // contributor tables of the tile-range phases (same partition as the kernel)
+    {
+      const int N3[3] = {qkv_rows, d.d_model, d.d_model};
+      const int K3[3] = {d.d_model, q_dim, d.d_ffn};
+      std::vector<uint16_t> tab(3 * 256, 0);
+      const long G = num_sms;
+      if (G > 255) return fail(SR_E_INVALID, "decode tables assume <= 255 SMs");
+      for (int t = 0; t < 3; ++t) {
+        const int tcol = std::min(K3[t], mk_tile_cols());
+        const long kt = (K3[t] + tcol - 1) / tcol, nb = (N3[t] + 31) / 32, T = kt * nb;
+        if (nb > 256) return fail(SR_E_INVALID, "decode tables hold <= 256 row blocks");
+        for (long b = 0; b < nb; ++b) {
+          const long u0 = b * kt, u1 = u0 + kt - 1;
+          // owner of unit u / first unit of CTA c under the kernel's partition
+          auto owner = [&](long u) { return T >= G ? ((u + 1) * G - 1) / T : u; };
+          auto first = [&](long c) { return T >= G ? T * c / G : std::min(c, T); };
+          const long c0 = owner(u0), c1 = owner(u1);
+          const long j0 = b - first(c0) / kt;
+          if (j0 >= L.mk_maxj || j0 > 15 || c1 - c0 + 1 > 15)
+            return fail(SR_E_INVALID, "decode partial tables out of range");
+          tab[t * 256 + b] = (uint16_t)(c0 | (c1 - c0 + 1) << 8 | j0 << 12);
+        }
+      }
+      SR_CK(cudaMemcpy(ws + L.mk_ctab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice));
+      mk.ctab = at<const uint16_t>(L.mk_ctab);
+      mk.attn_cnt = at<int>(L.mk_ctab + 3 * 256 * 2);
+    }
+    std::vector<MkLayer> ly(d.n_layers);
+    for (int l = 0; l < d.n_layers; ++l) ly[l] = MkLayer{lw(l, LN1), lw(l, BQKV), lw(l, LN2), nullptr};
+    SR_CK(cudaMemcpy(ws + L.mk_maps, maps.data(), n * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    SR_CK(cudaMemcpy(ws + L.mk_layers, ly.data(), ly.size() * sizeof(MkLayer),
+                     cudaMemcpyHostToDevice));
+    MkParams& p = mk;
+    p.maps = at<const CUtensorMap>(L.mk_maps);
+    p.layers = at<const MkLayer>(L.mk_layers);
+    p.embed = embed;
+    p.ln_f = ln_f;
+    p.rope = rope;
+    p.k_pool = k_pool;
+    p.v_pool = v_pool;
+    p.hA = at<float>(L.mk_h);
+    p.hB = p.hA + d.d_model;
+    const size_t pstride = (size_t)num_sms * L.mk_maxj * mk_tile_rows();
+    p.part_qkv = at<float>(L.mk_part);
+    p.part_o = p.part_qkv + pstride;
+    p.part_d = p.part_o + pstride;
+    p.apart = at<float>(L.mk_apart);
+    p.lm_part = at<float>(L.mk_lm);
+    p.act = act;
+    p.attn = attn;
+    p.st = st;
+    const char* pe = getenv("SR_MK_PROF");
+    p.prof = (pe && pe[0] == '1') ? at<unsigned long long>(L.mk_prof) : nullptr;
+    const char* te = getenv("SR_MK_TRACE");
+    p.trace = nullptr;
+    if (te && te[0] == '1') {  // bring-up aid: progress words readable after a hang
+      SR_CK(cudaHostAlloc((void**)&trace_host, (size_t)num_sms * 8 * 4, cudaHostAllocMapped));
+      memset(trace_host, 0, (size_t)num_sms * 8 * 4);
+      int* dptr = nullptr;
+      SR_CK(cudaHostGetDevicePointer((void**)&dptr, trace_host, 0));
+      p.trace = dptr;
+    }
+    p.L = d.n_layers;
+    p.d = d.d_model;
+    p.H = d.n_heads;
+    p.KV = d.n_kv_heads;
+    p.f = d.d_ffn;
+    p.vocab_rows = d.vocab_rows;
+    p.vocab_text = d.vocab_text;
+    p.n_pages = d.n_pages;
+    p.q_dim = q_dim;
+    p.kv_dim = kv_dim;
+    p.qkv_rows = qkv_rows;
+    p.eps = d.rms_eps;
+    p.maxj = L.mk_maxj;
+    const int tc = mk_tile_cols();
+    p.xs_elems = (std::max({d.d_model, q_dim, d.d_ffn}) + tc - 1) / tc * tc;
+    p.stages = mk_pick_stages(p.xs_elems);
+    // L2 prefetch run-ahead beyond the ring (tiles); off by default: measured
+    // slower on B200 (the extra HBM traffic delays the latency-bound phases)
+    p.l2_ahead = -1;
+    if (const char* v = getenv("SR_MK_L2AHEAD")) p.l2_ahead = atoi(v);
+    p.bar_sleep = 0;
+    p.evict_first = 1;
+    if (const char* v = getenv("SR_MK_EVICT_FIRST")) p.evict_first = atoi(v);
+    if (const char* v = getenv("SR_MK_BARSLEEP")) p.bar_sleep = atoi(v);
     return 0;
   }
 
@@ -502,7 +624,10 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
   for (auto& ev : m->ev) cudaEventCreate(&ev);
   if (const char* v = getenv("SR_NO_PDL")) m->pdl = (v[0] == '0');
   if (const char* v = getenv("SR_GEMM")) m->use_tc = strcmp(v, "mma") != 0;
-  if (const char* v = getenv("SR_DECODE")) m->stream_decode = strcmp(v, "stream") == 0;
+  if (const char* v = getenv("SR_DECODE")) {
+    m->stream_decode = strcmp(v, "stream") == 0;
+    m->graph_decode = strcmp(v, "graph") == 0;
+  }
   if (const char* v = getenv("SR_ATTN")) m->attn_simt = strcmp(v, "simt") == 0;
   if (const char* v = getenv("SR_PREFETCH")) m->prefetch = v[0] == '1';
   if (const char* v = getenv("SR_WATCH")) {
@@ -517,6 +642,10 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
     sr_model_destroy(m);
     return rc;
   }
+  if (int rc = m->build_mk()) {
+    sr_model_destroy(m);
+    return rc;
+  }
   *out_model = m;
   return 0;
 }
@@ -527,6 +656,7 @@ int sr_model_destroy(void* model) {
   if (m->exec) cudaGraphExecDestroy(m->exec);
   if (m->graph) cudaGraphDestroy(m->graph);
   if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
+  if (m->trace_host) cudaFreeHost(m->trace_host);
   for (auto& ev : m->ev)
     if (ev) cudaEventDestroy(ev);
   delete m;
@@ -571,7 +701,10 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
   p.counter = m->lm_ctr;
   SR_CK(gemv_launch(GEMV_LM_ARGMAX_X, p, m->num_sms, s, false));
   SR_CK(cudaEventRecord(m->ev[1], s));
-  if (!m->stream_decode) {
+  if (!m->stream_decode && !m->graph_decode) {
+    // one persistent kernel decodes the whole step (decode_mk.cu)
+    SR_CK(mk_launch(m->mk, m->num_sms, s));
+  } else if (m->graph_decode) {
     SR_CK(cudaGraphLaunch(m->exec, s));
   } else {
     // profiling mode (SR_DECODE=stream): same kernels launched per token from
@@ -664,6 +797,23 @@ int sr_forward_logits(void* model, const int32_t* page_table, int32_t start_pos,
       SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
     }
   }
+  return 0;
+}
+
+int sr_debug_profile(void* model, uint64_t* h_out, int32_t n) {
+  Model* m = (Model*)model;
+  if (!m || !h_out || n < 0) return fail(SR_E_INVALID, "null argument");
+  if (n > SR_PROF_EVENTS) n = SR_PROF_EVENTS;
+  SR_CK(cudaDeviceSynchronize());
+  SR_CK(cudaMemcpy(h_out, m->ws + m->L.mk_prof, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int sr_debug_trace(void* model, int32_t* h_out, int32_t n) {
+  Model* m = (Model*)model;
+  if (!m || !h_out || !m->trace_host) return fail(SR_E_INVALID, "tracing is off (SR_MK_TRACE=1)");
+  const int cap = m->num_sms * 8;
+  for (int i = 0; i < n && i < cap; ++i) h_out[i] = ((volatile int*)m->trace_host)[i];
   return 0;
 }
 
