@@ -247,8 +247,9 @@ def run_ours(args) -> None:
                  "draft_decode_ms_per_token": round(ds.decode_ms / max(1, ds.decode_tokens), 4),
                  "base_decode_ms_per_token": round(db.decode_ms / max(1, db.decode_tokens), 4),
                  "base_prefill_tokens": db.prefill_tokens, "base_prefill_ms": round(db.prefill_ms, 2)},
-        "roofline": {"kernel": "base fallback decode step (CUDA graph: 5 GEMV/attention kernels per "
-                               "layer + LM-head argmax, device-side loop)",
+        "roofline": {"kernel": "decode_mk_kernel (persistent weight-streaming decode, base model "
+                               "fallback steps): algorithmic bytes = 2*(P_body+P_head) + (C+1)*kvB "
+                               "per token (SURVEY 8d) / CUDA-event decode time",
                      "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
                      "peak_source": peaks["src"], "traffic": None,

@@ -155,8 +155,9 @@ class EngineStats:
         ctx0 = start + n_ids
         for i in range(steps):
             self.decode_bytes += spec.decode_bytes(ctx0 + i)
-        self.launches += (self._prefill_launches(spec, n_ids) + 2 + 1
-                          + steps * (5 * spec.n_layers + 1))
+        # decode_begin + prefill + first-token LM head + one persistent decode
+        # kernel for the whole step (decode_mk.cu)
+        self.launches += self._prefill_launches(spec, n_ids) + 3
         self.h2d_bytes += 4 * n_ids + 64
         self.d2h_bytes += 4 * (2 + m.max_new) * 2
 

@@ -351,7 +351,7 @@ SR_DEV void mk_load_page(const MkParams& p, int layer, int g, int page, int nval
 // ticket) merges all splits of g into the bf16 attention output.
 SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_table,
                          const __nv_bfloat16* bias, const uint16_t* tab, int c, int S_a,
-                         int npages, float* sm, int* s_flag) {
+                         int npages, float* sm) {
   const int Gq = p.H / p.KV;
   const int g = c / S_a, s = c % S_a;
   if (g >= p.KV) return;  // uniform per CTA
@@ -369,6 +369,11 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
   const int posl = warp * 4 + (lane >> 3), sub = lane & 7;
   const int dd = tid % kHeadDim, grp = tid / kHeadDim;
 
+  const bool sub_prof = p.prof && c == 0 && tid == 0 && layer == 1;
+  int sev = 0;
+#define SUB_EV() \
+  do { if (sub_prof && sev < 32) p.prof[1600 + sev++] = global_ns(); } while (0)
+  SUB_EV();
   // first page's K/V loads go out before anything else (independent of q)
   PageRegs cur;
   {
@@ -414,6 +419,7 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
 #pragma unroll
   for (int j = 0; j < kMkMaxGq; ++j) acc[j] = 0.f;
   cbar();
+  SUB_EV();  // q / new k,v ready
 
   for (int pg_i = p0; pg_i < p1; ++pg_i) {
     const int P0 = pg_i * kPage;
@@ -462,6 +468,7 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
       }
     }
     cbar();
+    SUB_EV();  // scores
     if (warp < Gq) {  // online softmax of head `warp` over this page
       const int j = warp;
       const float s0 = ps[j * 64 + lane], s1 = ps[j * 64 + lane + 32];
@@ -524,54 +531,52 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
     p.apart[((size_t)c * kMkMaxGq + tid) * 130 + 128] = mrun[tid];
     p.apart[((size_t)c * kMkMaxGq + tid) * 130 + 129] = lrun[tid];
   }
-  // last split of kv head g merges the splits (classic last-block pattern)
-  cbar();
-  if (tid == 0) {
-    __threadfence();
-    const int ticket = atomicAdd(p.attn_cnt + g, 1);
-    const int last = ticket == S_a - 1;
-    if (last) p.attn_cnt[g] = 0;  // re-armed for the next layer (after a grid barrier)
-    __threadfence();
-    *s_flag = last;
-  }
-  cbar();
-  if (!*s_flag) return;
-  // merge: (m, l) of every split and head into shared memory, per-head
-  // weights exp2(m_s - M) / L, then one weighted sum per output element
-  float* ml = sm;                      // [S_a][Gq][2] (reuses qs / ps)
-  float* wts = red;                    // [S_a][Gq]
-  for (int t = tid; t < S_a * Gq; t += kMkConsumers) {
-    const int q = t / Gq, j = t - q * Gq;
-    const float* a = p.apart + ((size_t)(g * S_a + q) * kMkMaxGq + j) * 130;
-    ml[2 * t] = __ldcg(a + 128);
-    ml[2 * t + 1] = __ldcg(a + 129);
-  }
-  cbar();
-  if (warp < Gq) {
-    const int j = warp;
-    float M = -INFINITY;
-    for (int q = lane; q < S_a; q += 32) M = fmaxf(M, ml[2 * (q * Gq + j)]);
-    M = warp_max(M);
-    float Ls = 0.f;
-    for (int q = lane; q < S_a; q += 32) {
-      const float w = exp2f(ml[2 * (q * Gq + j)] - M);
-      wts[q * Gq + j] = w;
-      Ls += w * ml[2 * (q * Gq + j) + 1];
+  SUB_EV();  // partial written
+#undef SUB_EV
+}
+
+// COMBINE: merge the attention splits.  Work item = (query head, 32-dim slice),
+// spread over the grid; 16 thread groups each take every 16th split, one
+// round trip of loads, then a fixed-order merge of the groups (deterministic).
+SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, float* sm) {
+  const int Gq = p.H / p.KV;
+  const int tid = threadIdx.x, dl = tid & 31, grp = tid >> 5;
+  float* r_o = sm;               // [16][32]
+  float* r_m = sm + 16 * 32;     // [16]
+  float* r_l = r_m + 16;         // [16]
+  for (int it = c; it < p.H * 4; it += G) {
+    const int h = it >> 2, d = (it & 3) * 32 + dl;
+    const int g = h / Gq, j = h - g * Gq;
+    float m = -INFINITY, l = 0.f, o = 0.f;
+    for (int q = grp; q < S_a; q += kMkWarps) {
+      const float* a = p.apart + ((size_t)(g * S_a + q) * kMkMaxGq + j) * 130;
+      const float ms = __ldcg(a + 128), ls = __ldcg(a + 129), os = __ldcg(a + d);
+      const float mn = fmaxf(m, ms);
+      const float x = exp2f(m - mn), y = exp2f(ms - mn);
+      l = l * x + ls * y;
+      o = o * x + os * y;
+      m = mn;
     }
-    Ls = warp_sum(Ls);
-    __syncwarp();
-    const float inv = 1.f / Ls;
-    for (int q = lane; q < S_a; q += 32) wts[q * Gq + j] *= inv;
-  }
-  cbar();
-  for (int o = tid; o < Gq * kHeadDim; o += kMkConsumers) {
-    const int j = o / kHeadDim, d2 = o - j * kHeadDim;
-    const float* a = p.apart + ((size_t)(g * S_a) * kMkMaxGq + j) * 130 + d2;
-    float acc_o = 0.f;
-#pragma unroll 16
-    for (int q = 0; q < S_a; ++q)
-      acc_o = fmaf(wts[q * Gq + j], __ldcg(a + (size_t)q * kMkMaxGq * 130), acc_o);
-    p.attn[(size_t)(g * Gq + j) * kHeadDim + d2] = __float2bfloat16_rn(acc_o);
+    r_o[grp * 32 + dl] = o;
+    if (dl == 0) {
+      r_m[grp] = m;
+      r_l[grp] = l;
+    }
+    cbar();
+    if (grp == 0) {
+      float M = r_m[0], L = r_l[0], O = r_o[dl];
+      for (int q = 1; q < kMkWarps; ++q) {
+        const float mq = r_m[q];
+        if (mq == -INFINITY) continue;
+        const float mn = fmaxf(M, mq);
+        const float x = exp2f(M - mn), y = exp2f(mq - mn);
+        L = L * x + r_l[q] * y;
+        O = O * x + r_o[q * 32 + dl] * y;
+        M = mn;
+      }
+      p.attn[(size_t)h * kHeadDim + d] = __float2bfloat16_rn(O / L);
+    }
+    cbar();
   }
 }
 
@@ -617,6 +622,32 @@ struct MkCursor {
   SR_DEV int col() const { return kk * tc; }
   SR_DEV int row() const { return bb * kTR; }
 };
+
+SR_DEV void l2_prefetch(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
+// Layer l's small vectors (norm weights, qkv bias) and this CTA's attention
+// pages, pulled into L2 a layer early: under the weight stream an HBM miss
+// costs several microseconds on the latency-bound path (l == L: next token).
+SR_DEV void mk_prefetch_next_layer(const MkParams& p, int l, int pos, const int* page_table,
+                                   int c, int G, int S_a, int npages) {
+  if (l >= p.L) l = 0;
+  if (c == 0) {
+    const MkLayer ly = p.layers[l];
+    l2_prefetch(ly.ln1, p.d * 2);
+    l2_prefetch(ly.ln2, p.d * 2);
+    l2_prefetch(ly.bqkv, p.qkv_rows * 2);
+  }
+  const int g = c / S_a, s = c % S_a;
+  if (g >= p.KV) return;
+  const int p0 = (int)((long long)npages * s / S_a), p1 = (int)((long long)npages * (s + 1) / S_a);
+  for (int pg = p0; pg < p1; ++pg) {
+    const size_t off = kv_offset(l, page_table[pg], g, 0, p.n_pages, p.KV);
+    l2_prefetch(p.k_pool + off, kPage * kHeadDim * 2);
+    l2_prefetch(p.v_pool + off, kPage * kHeadDim * 2);
+  }
+}
 
 __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams p) {
   extern __shared__ __align__(1024) uint8_t mk_smem[];
@@ -750,7 +781,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
     const int npages = pos / kPage + 1;
     // splits per kv head: every CTA busy at long context, >= 2 pages per split
     int S_a = G / p.KV;
-    if (S_a > (npages + 1) / 2) S_a = (npages + 1) / 2;
+    if (S_a > (npages + p.min_pages - 1) / p.min_pages) S_a = (npages + p.min_pages - 1) / p.min_pages;
     if (S_a < 1) S_a = 1;
     Top2 best;
     best.init();
@@ -767,10 +798,21 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 3 sync
       // attention (+ merge of the splits by the last split CTA of each kv head)
-      mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, npages, scratch, &s_flag);
+      const uint64_t ta0 = global_ns();
+      mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, npages, scratch);
+      if (p.prof && threadIdx.x == 0 && l == 1 && tstep < 40) {  // per-CTA attention time, layer 1
+        p.prof[1024 + c] = global_ns() - ta0;
+        p.prof[1024 + 256 + c] = (c % S_a) == S_a - 1;
+      }
+      // warm L2 with what the next layer reads on its latency-bound path
+      if (threadIdx.x == 0) mk_prefetch_next_layer(p, l + 1, pos, page_table, c, G, S_a, npages);
       MK_EV();  // 4 attention
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 5 sync
+      mk_combine(p, c, G, S_a, scratch);
+      MK_EV();  // 6 combine
+      mk_grid_sync(bar, target, G, p.bar_sleep);
+      MK_EV();  // 7 sync
       // O
       mk_stage_vec(p.attn, p.q_dim, xs);
       MK_EV();  // 8 stage

@@ -208,6 +208,7 @@ struct MkParams {
   int l2_ahead;              // tiles prefetched into L2 beyond the shared-memory ring
   int bar_sleep;             // ns of backoff between grid-barrier polls
   int evict_first;           // stream weights with an L2 evict-first policy
+  int min_pages;             // attention: minimum K/V pages per split
 };
 
 size_t mk_smem_bytes(int stages, int xs_elems);

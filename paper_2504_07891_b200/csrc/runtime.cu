@@ -253,6 +253,8 @@ struct Model {
     if (const char* v = getenv("SR_MK_L2AHEAD")) p.l2_ahead = atoi(v);
     p.bar_sleep = 0;
     p.evict_first = 1;
+    p.min_pages = 1;
+    if (const char* v = getenv("SR_MK_MINPAGES")) p.min_pages = std::max(1, atoi(v));
     if (const char* v = getenv("SR_MK_EVICT_FIRST")) p.evict_first = atoi(v);
     if (const char* v = getenv("SR_MK_BARSLEEP")) p.bar_sleep = atoi(v);
     return 0;

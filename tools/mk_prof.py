@@ -19,7 +19,8 @@ os.environ["SR_MK_PROF"] = "1"
 
 import torch  # noqa: E402
 
-NAMES = ["qkv_prologue", "qkv_gemv", "sync_qkv", "attention", "sync_attn", "o_stage",
+NAMES = ["qkv_prologue", "qkv_gemv", "sync_qkv", "attention", "sync_attn", "combine", "sync_comb",
+         "o_stage",
          "o_gemv", "sync_o", "gu_prologue", "gu_gemv", "sync_gu", "d_stage", "d_gemv", "sync_d"]
 E = len(NAMES)
 
@@ -63,6 +64,17 @@ def main() -> None:
                     "sync": round((tail[2] - tail[1]) / 1e3, 2),
                     "select": round((tail[3] - tail[2]) / 1e3, 2)}
     out["token_us"] = round((t[n - 1] - t[0]) / 1e3, 1)
+    import statistics
+    att = ev[1024:1024 + 148]
+    last = ev[1280:1280 + 148]
+    busy = [x / 1e3 for x in att if x > 0]
+    if busy:
+        out["attn_cta_us"] = {"n": len(busy), "min": round(min(busy), 2),
+                              "median": round(statistics.median(busy), 2),
+                              "max": round(max(busy), 2),
+                              "last_split_max": round(max([x / 1e3 for x, f in zip(att, last) if f] or [0]), 2)}
+    sub = [x for x in ev[1600:1632] if x > 0]
+    out["attn_cta0_steps_us"] = [round((b - a) / 1e3, 2) for a, b in zip(sub, sub[1:])]
     out["model"] = a.model
     out["ctx"] = a.ctx
     print(json.dumps(out), flush=True)
