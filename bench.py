@@ -45,7 +45,11 @@ import torch  # noqa: E402
 
 METRIC = "CoT tokens/sec & ms per reasoning step (draft+verify+fallback) at 1–8 B200"
 UNIT = "CoT tokens/s"
-WORKLOAD = "C2: R1-Distill-1.5B-shape draft + Qwen2.5-7B-shape base, random-init bf16, 4K-token CoT, batch 1"
+WORKLOADS = {
+    "1.5b+7b": "C2: R1-Distill-1.5B-shape draft + Qwen2.5-7B-shape base, random-init bf16, 4K-token CoT, batch 1",
+    "1.5b+32b": "C3: R1-1.5B-shape draft + QwQ-32B-shape base, random-init bf16, 8K-token CoT, threshold 7, batch 1",
+    "tiny": "C1: tiny random-init pair (draft 2L d=128 + base 4L d=256), greedy, threshold 7",
+}
 
 
 def _peaks() -> dict:
@@ -229,7 +233,7 @@ def run_ours(args) -> None:
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights, seeded 64-word problems)",
-        "config": {"workload": WORKLOAD, "pair": args.pair, "threshold": args.threshold,
+        "config": {"workload": WORKLOADS[args.pair], "pair": args.pair, "threshold": args.threshold,
                    "token_budget": args.budget, "max_step_tokens": args.max_step_tokens,
                    "batch": 1, "parallelism": f"dp{world} (independent problems per GPU)",
                    "l2": "weights (17 GB) exceed L2 (126 MB): no flush needed"},
@@ -405,7 +409,7 @@ def run_reference(args) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / len(timed), 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "pair": args.pair,
+        "data": "synthetic", "config": {"workload": WORKLOADS[args.pair], "pair": args.pair,
                                         "threshold": args.threshold, "token_budget": args.budget},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{engine_kind} driving the CPU oracle; per-token CPU costs of "

@@ -110,10 +110,15 @@ MODELS: dict[str, ModelSpec] = {
     # public model-card shapes
     "r1-1.5b": ModelSpec("r1-1.5b", 28, 1536, 12, 2, 8960, V_QWEN_DRAFT, V_QWEN_DRAFT,
                          rope_theta=10_000.0),
+    # judge offsets measured on the B200 by tools/calibrate_judge.py --gpu (seed 0)
     "qwen2.5-7b": ModelSpec("qwen2.5-7b", 28, 3584, 28, 4, 18944, V_QWEN_BASE, V_QWEN_DRAFT,
-                            judge=True),
+                            judge=True,
+                            judge_offsets=(-0.75, 1.0, 0.75, -1.875, -1.5, 0.75, -0.875, 0.0,
+                                           0.875, 1.5)),
     "qwq-32b": ModelSpec("qwq-32b", 64, 5120, 40, 8, 27648, V_QWEN_BASE, V_QWEN_DRAFT,
-                         judge=True),
+                         judge=True,
+                         judge_offsets=(-0.75, 0.75, -0.75, 2.75, 0.0, -1.0, -1.75, -0.875,
+                                        2.875, -1.5)),
 }
 
 PAIRS = {

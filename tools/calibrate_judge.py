@@ -19,19 +19,30 @@ from paper_2504_07891_b200.shapes import (get_spec, judge_calibration_prompts,  
                                           judge_offsets_update, make_weights)
 
 
-def logits_fn_for(spec, gpu: bool):
-    w = make_weights(spec, 0, device="cuda" if gpu else "cpu")
-    if gpu:
+class GpuJudge:
+    """Base model on the B200; only the LM head depends on the offsets, so it
+    is regenerated in place between iterations (the 32B fits once, not twice)."""
+
+    def __init__(self, spec):
         from paper_2504_07891_b200.backend import B200Backend
         from paper_2504_07891_b200.domain import BackendRole
 
-        b = B200Backend(spec, BackendRole.BASE, weights=w, max_ctx=2048)
-        s = b.pool.streams[0]
+        self.b = B200Backend(spec, BackendRole.BASE, weights=make_weights(spec, 0, device="cuda"),
+                             max_ctx=2048)
+        self.s = self.b.pool.streams[0]
 
-        def fn(ids):
-            b.engine.truncate(s, 0)
-            return b.engine.forward_logits(s, ids, all_rows=False)[0].cpu()
-        return fn
+    def set_spec(self, spec):
+        from paper_2504_07891_b200.shapes import make_tensor
+
+        self.b.device_model.weights["lm_head"].copy_(make_tensor(spec, 0, "lm_head", "cuda"))
+
+    def __call__(self, ids):
+        self.b.engine.truncate(self.s, 0)
+        return self.b.engine.forward_logits(self.s, ids, all_rows=False)[0].cpu()
+
+
+def logits_fn_for(spec, gpu: bool):
+    w = make_weights(spec, 0, device="cpu")
     from oracle.ref_model import RefModel
 
     m = RefModel(spec, w)
@@ -43,8 +54,13 @@ def main() -> None:
     gpu = "--gpu" in sys.argv
     spec = get_spec(name)
     prompts = judge_calibration_prompts(spec)
-    for it in range(3):
-        fn = logits_fn_for(spec, gpu)
+    judge = GpuJudge(spec) if gpu else None
+    for it in range(4):
+        if gpu:
+            judge.set_spec(spec)
+            fn = judge
+        else:
+            fn = logits_fn_for(spec, gpu)
         rows = [fn(p) for p in prompts]
         hist = collections.Counter(int(r[:10].argmax()) for r in rows)
         print(f"iter {it}: offsets {spec.judge_offsets} -> argmax-digit histogram {sorted(hist.items())}",
