@@ -72,7 +72,8 @@ constexpr int kMkProfEvents = SR_PROF_EVENTS;
 constexpr int kMkNorm = 5120 / kMkConsumers;
 constexpr int kMkAttnScratchFloats =
     kMkMaxGq * 128 + kMkMaxGq * 64 + 3 * kMkMaxGq + 4 * kMkMaxGq * 128 + 2 * 128;
-constexpr int kMkTab = 256;  // max 32-row blocks of a tile-range phase (smem tables)
+constexpr int kMkTab = 256;
+constexpr int kKvBufBytes = 2 * kPage * kHeadDim * 2;  // 32 KB  // max 32-row blocks of a tile-range phase (smem tables)
 
 enum { PH_QKV = 0, PH_O = 1, PH_GU = 2, PH_D = 3, PH_LM = 4 };
 
@@ -323,27 +324,15 @@ SR_DEV float mk_qkv_val(const MkParams& p, const __nv_bfloat16* bias, const uint
   return mk_sum_parts(p.part_qkv, tab, row, p.maxj) + bf_to_f(bias[row]);
 }
 
-// K/V of one page held in registers: 8 lanes per position x 16 dims of K
-// (scores), one thread per (dim, 16-position group) of V (P.V)
-struct PageRegs {
-  uint4 k0, k1;
-  __nv_bfloat16 v[16];
-};
-
-SR_DEV void mk_load_page(const MkParams& p, int layer, int g, int page, int nval, int posl,
-                         int sub, int dd, int grp, PageRegs& r) {
-  if (posl < nval) {
-    const uint4* kr = reinterpret_cast<const uint4*>(
-        p.k_pool + kv_offset(layer, page, g, posl, p.n_pages, p.KV) + sub * 16);
-    r.k0 = __ldcg(kr);
-    r.k1 = __ldcg(kr + 1);
-  }
-  const __nv_bfloat16* vb = p.v_pool + kv_offset(layer, page, g, 0, p.n_pages, p.KV) + dd;
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int pl = grp * 16 + q;
-    if (pl < nval) r.v[q] = __ldcg(vb + (size_t)pl * kHeadDim);
-  }
+// one K page + one V page (16 KB each, contiguous in the pools) -> shared
+// memory with two 1-D bulk copies on one mbarrier (issued by thread 0)
+SR_DEV void mk_fetch_page(const MkParams& p, int layer, int g, int page, uint8_t* kvbuf,
+                          uint64_t* kvbar) {
+  const size_t off = kv_offset(layer, page, g, 0, p.n_pages, p.KV);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(kvbar, 2 * kPage * kHeadDim * 2);
+  bulk_load_1d(kvbuf, p.k_pool + off, kPage * kHeadDim * 2, kvbar);
+  bulk_load_1d(kvbuf + kPage * kHeadDim * 2, p.v_pool + off, kPage * kHeadDim * 2, kvbar);
 }
 
 // Attention of kv head g over pages [p0, p1) for its Gq query heads; the split
@@ -351,7 +340,7 @@ SR_DEV void mk_load_page(const MkParams& p, int layer, int g, int page, int nval
 // ticket) merges all splits of g into the bf16 attention output.
 SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_table,
                          const __nv_bfloat16* bias, const uint16_t* tab, int c, int S_a,
-                         int npages, float* sm) {
+                         int npages, float* sm, uint8_t* kvbuf, uint64_t* kvbar, uint32_t& kvpar) {
   const int Gq = p.H / p.KV;
   const int g = c / S_a, s = c % S_a;
   if (g >= p.KV) return;  // uniform per CTA
@@ -374,19 +363,20 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
 #define SUB_EV() \
   do { if (sub_prof && sev < 32) p.prof[1600 + sev++] = global_ns(); } while (0)
   SUB_EV();
-  // first page's K/V loads go out before anything else (independent of q)
-  PageRegs cur;
-  {
-    const int nval = min(kPage, pos + 1 - p0 * kPage);
-    mk_load_page(p, layer, g, page_table[p0], nval, posl, sub, dd, grp, cur);
-  }
+  // first page's K/V copy goes out before anything else (independent of q)
+  if (tid == 0) mk_fetch_page(p, layer, g, page_table[p0], kvbuf, kvbar);
+  const __nv_bfloat16* ks = reinterpret_cast<const __nv_bfloat16*>(kvbuf);
+  const __nv_bfloat16* vs = ks + kPage * kHeadDim;
   for (int t = tid; t < Gq * kHalf; t += kMkConsumers) {
     const int j = t / kHalf, i = t % kHalf;
     const int r0 = (g * Gq + j) * kHeadDim + i;
     const float v0 = mk_qkv_val(p, bias, tab, r0), v1 = mk_qkv_val(p, bias, tab, r0 + kHalf);
     const float cs = p.rope[((size_t)pos * kHalf + i) * 2], sn = p.rope[((size_t)pos * kHalf + i) * 2 + 1];
-    qs[j * 128 + i] = round_bf16(v0 * cs - v1 * sn);
-    qs[j * 128 + i + kHalf] = round_bf16(v1 * cs + v0 * sn);
+    // layout [head][e4][sub][4]: dim = sub*16 + e4*4 + k, so the 8 lanes of a
+    // position group read 8 consecutive float4 (conflict-free)
+    const int i2 = i + kHalf;
+    qs[j * 128 + ((i & 15) >> 2) * 32 + (i >> 4) * 4 + (i & 3)] = round_bf16(v0 * cs - v1 * sn);
+    qs[j * 128 + ((i2 & 15) >> 2) * 32 + (i2 >> 4) * 4 + (i2 & 3)] = round_bf16(v1 * cs + v0 * sn);
   }
   const bool has_new = p1 == npages;
   if (has_new) {  // new position: k / v from the partials; appended to the pool
@@ -425,6 +415,9 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
     const int P0 = pg_i * kPage;
     const int nval = min(kPage, pos + 1 - P0);
     const int newl = has_new && pg_i == p1 - 1 ? pos - P0 : -1;  // slot of the new position
+    mbar_wait(kvbar, kvpar);
+    kvpar ^= 1u;
+    SUB_EV();  // page landed
     // scores: 8 lanes per position, 16 dims per lane
     {
       float sc[kMkMaxGq];
@@ -436,8 +429,9 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
 #pragma unroll
           for (int e = 0; e < 16; ++e) kf[e] = kn[sub * 16 + e];
         } else {
-          const uint32_t kw[8] = {cur.k0.x, cur.k0.y, cur.k0.z, cur.k0.w,
-                                  cur.k1.x, cur.k1.y, cur.k1.z, cur.k1.w};
+          const uint4* kr = reinterpret_cast<const uint4*>(ks + posl * kHeadDim + sub * 16);
+          const uint4 k0 = kr[0], k1 = kr[1];
+          const uint32_t kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const float2 f2 = bf2_to_f2(kw[e]);
@@ -448,10 +442,15 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
 #pragma unroll
         for (int j = 0; j < kMkMaxGq; ++j) {
           if (j < Gq) {
-            const float* q = qs + j * 128 + sub * 16;
             float a = 0.f;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) a = fmaf(q[e], kf[e], a);
+            for (int e4 = 0; e4 < 4; ++e4) {
+              const float4 q4 = *reinterpret_cast<const float4*>(qs + j * 128 + e4 * 32 + sub * 4);
+              a = fmaf(q4.x, kf[4 * e4], a);
+              a = fmaf(q4.y, kf[4 * e4 + 1], a);
+              a = fmaf(q4.z, kf[4 * e4 + 2], a);
+              a = fmaf(q4.w, kf[4 * e4 + 3], a);
+            }
             sc[j] = a;
           }
         }
@@ -491,30 +490,34 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
     {
       float vf[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) vf[q] = bf_to_f(cur.v[q]);
+      for (int q = 0; q < 16; ++q) vf[q] = bf_to_f(vs[(grp * 16 + q) * kHeadDim + dd]);
       if (newl >= grp * 16 && newl < grp * 16 + 16) {
 #pragma unroll
         for (int q = 0; q < 16; ++q)
           if (grp * 16 + q == newl) vf[q] = vn[dd];
       }
-      if (pg_i + 1 < p1) {  // next page's loads overlap this page's P.V
-        const int nv2 = min(kPage, pos + 1 - (pg_i + 1) * kPage);
-        mk_load_page(p, layer, g, page_table[pg_i + 1], nv2, posl, sub, dd, grp, cur);
-      }
 #pragma unroll
       for (int j = 0; j < kMkMaxGq; ++j)
         if (j < Gq) acc[j] *= alph[j];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int pl = grp * 16 + q;
-        if (pl < nval) {
+      for (int q = 0; q < 16; ++q)
+        if (grp * 16 + q >= nval) vf[q] = 0.f;  // slots past the context may hold garbage
 #pragma unroll
-          for (int j = 0; j < kMkMaxGq; ++j)
-            if (j < Gq) acc[j] = fmaf(ps[j * 64 + pl], vf[q], acc[j]);
+      for (int j = 0; j < kMkMaxGq; ++j) {
+        if (j < Gq) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 pp = *reinterpret_cast<const float4*>(ps + j * 64 + grp * 16 + q4 * 4);
+            acc[j] = fmaf(pp.x, vf[4 * q4], acc[j]);
+            acc[j] = fmaf(pp.y, vf[4 * q4 + 1], acc[j]);
+            acc[j] = fmaf(pp.z, vf[4 * q4 + 2], acc[j]);
+            acc[j] = fmaf(pp.w, vf[4 * q4 + 3], acc[j]);
+          }
         }
       }
     }
-    cbar();
+    cbar();  // page buffer free
+    if (pg_i + 1 < p1 && tid == 0) mk_fetch_page(p, layer, g, page_table[pg_i + 1], kvbuf, kvbar);
   }
 #pragma unroll
   for (int j = 0; j < kMkMaxGq; ++j)
@@ -632,7 +635,11 @@ SR_DEV void l2_prefetch(const void* ptr, uint32_t bytes) {
 // costs several microseconds on the latency-bound path (l == L: next token).
 SR_DEV void mk_prefetch_next_layer(const MkParams& p, int l, int pos, const int* page_table,
                                    int c, int G, int S_a, int npages) {
-  if (l >= p.L) l = 0;
+  if (l >= p.L) {  // layer 0 of the next token: its RoPE row too
+    l = 0;
+    ++pos;
+  }
+  if (c == 1) l2_prefetch(p.rope + (size_t)pos * kHalf * 2, kHalf * 2 * 4);
   if (c == 0) {
     const MkLayer ly = p.layers[l];
     l2_prefetch(ly.ln1, p.d * 2);
@@ -660,6 +667,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   __shared__ int s_flag;
   __shared__ uint16_t s_tab[3][kMkTab];  // contributor tables: qkv, o, down
   __shared__ PhaseInfo s_ph[5];
+  __shared__ __align__(8) uint64_t kvbar;
   __shared__ float s_margin;
   __shared__ volatile int s_stop;
 
@@ -667,7 +675,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = mk_smem;
-  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(mk_smem + (size_t)S * kStageBytes);
+  uint8_t* kvbuf = mk_smem + (size_t)S * kStageBytes;  // one K page + one V page
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(kvbuf + kKvBufBytes);
   float* scratch = reinterpret_cast<float*>(xs);
 
   if (threadIdx.x == 0) {
@@ -676,6 +685,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       mbar_init(&empty[i], kMkWarps);
     }
     s_stop = 0;
+    mbar_init(&kvbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < 5) s_ph[threadIdx.x] = mk_phase_info(p, threadIdx.x, blockIdx.x, gridDim.x);
@@ -756,6 +766,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   unsigned* bar = &st->bar;
   unsigned target = 0;
   RingPos rp{0, 0u};
+  uint32_t kvpar = 0u;
   const int Gq = p.H / p.KV;
   (void)Gq;
   bool done = st->done != 0;
@@ -799,7 +810,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       MK_EV();  // 3 sync
       // attention (+ merge of the splits by the last split CTA of each kv head)
       const uint64_t ta0 = global_ns();
-      mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, npages, scratch);
+      mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, npages, scratch, kvbuf,
+                   &kvbar, kvpar);
       if (p.prof && threadIdx.x == 0 && l == 1 && tstep < 40) {  // per-CTA attention time, layer 1
         p.prof[1024 + c] = global_ns() - ta0;
         p.prof[1024 + 256 + c] = (c % S_a) == S_a - 1;
@@ -911,7 +923,7 @@ size_t mk_smem_bytes(int stages, int xs_elems) {
   size_t xs = (size_t)xs_elems * 2;
   const size_t attn = (size_t)kMkAttnScratchFloats * 4;
   if (xs < attn) xs = attn;
-  return (size_t)stages * kStageBytes + xs;
+  return (size_t)stages * kStageBytes + kKvBufBytes + xs;
 }
 
 int mk_pick_stages(int xs_elems) {

@@ -61,6 +61,15 @@ SR_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, i
       : "memory");
 }
 
+// contiguous global -> shared bulk copy completing on an mbarrier
+SR_DEV void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // fire-and-forget L2 prefetch of one tensor-map box
 SR_DEV void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(map), "r"(c0),

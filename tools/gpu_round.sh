@@ -1,4 +1,4 @@
-timeout 900 python bench.py --steps 30 --warmup 3 > gpurun_out/bench_c2.log 2>&1
-tail -1 gpurun_out/bench_c2.log | cut -c1-1500
-timeout 1200 python bench.py --pair 1.5b+32b --budget 8192 --steps 12 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.log 2>&1
-tail -3 gpurun_out/bench_c3.log | cut -c1-1500
+timeout 300 python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -2
+for m in r1-1.5b qwen2.5-7b; do
+timeout 300 python tools/mk_prof.py $m --ctx 2048 > gpurun_out/mkprof_$m.log 2>&1
+done
