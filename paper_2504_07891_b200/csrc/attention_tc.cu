@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams
       }
     }
   }
-  if (nsplit == 1) return;
+  if (nsplit == 1 || p.sep_merge) return;  // sep_merge: attn_merge_kernel merges
 
   // ---- split merge: last CTA of (kv head, query tile) ----
   __threadfence();
@@ -356,6 +356,47 @@ __global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams
     __nv_bfloat16* o = const_cast<__nv_bfloat16*>(q_row_ptr(p, G, g, row0 + rr)) - p.q + p.out;
     o[d] = __float2bfloat16_rn(A);
   }
+}
+
+// Split merge for prefill as its own grid-wide kernel: thread = (query row,
+// dim); fixed split order (deterministic).  A single last CTA per query tile
+// would read every split of 64 rows serially.
+__global__ void __launch_bounds__(512) attn_merge_kernel(AttnParams p, int M_rows, int G,
+                                                         int nsplit) {
+  grid_launch_dependents();
+  grid_wait();
+  const int g = blockIdx.y;
+  const int r = blockIdx.x * 4 + (threadIdx.x >> 7), d = threadIdx.x & 127;
+  if (r >= M_rows) return;
+  constexpr size_t ps = kHeadDim + 2;
+  const float* base = p.part + (size_t)g * M_rows * nsplit * ps + (size_t)r * nsplit * ps;
+  float M = -INFINITY;
+  for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, base[sp * ps + kHeadDim]);
+  float L = 0.f, A = 0.f;
+#pragma unroll 4
+  for (int sp = 0; sp < nsplit; ++sp) {
+    const float ms = base[sp * ps + kHeadDim];
+    const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+    L = fmaf(w, base[sp * ps + kHeadDim + 1], L);
+    A = fmaf(w, base[sp * ps + d], A);
+  }
+  __nv_bfloat16* o = const_cast<__nv_bfloat16*>(q_row_ptr(p, G, g, r)) - p.q + p.out;
+  o[d] = __float2bfloat16_rn(L > 0.f ? A / L : 0.f);
+}
+
+cudaError_t attn_merge_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream) {
+  const int G = p.n_heads / p.n_kv;
+  const int M_rows = M_tokens * G;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((M_rows + 3) / 4, p.n_kv);
+  cfg.blockDim = dim3(512);
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, attn_merge_kernel, p, M_rows, G, nsplit);
 }
 
 // ----------------------------------------------------------------- decode --
@@ -619,7 +660,7 @@ cudaError_t attn_decode_tc_launch(const AttnParams& p, cudaStream_t stream, bool
 
 int attn_tc_splits(int n_kv, int q_tiles, int T, int num_sms) {
   const int tiles = (T + kTile - 1) / kTile;
-  int s = num_sms / (n_kv * q_tiles);
+  int s = 2 * num_sms / (n_kv * q_tiles);  // two CTAs per SM (81 KB smem each)
   if (s > tiles) s = tiles;
   if (s > kAttnMaxSplit) s = kAttnMaxSplit;
   return s < 1 ? 1 : s;

@@ -111,10 +111,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
+  grid_launch_dependents();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    for (int i = 0; i < nkb; ++i) {
+    // Weights do not depend on the previous kernel: the first ring's worth of
+    // weight tiles is requested before the programmatic-dependency wait, so
+    // it overlaps the predecessor's tail; activations are loaded after it.
+    const int pre = nkb < stages ? nkb : stages;
+    for (int i = 0; i < pre; ++i) {
+      uint8_t* sw = base + (size_t)i * kStageBytes;
+      mbar_expect_tx(&full_bar[i], kStageBytes);
+      tma_load_2d(sw, &tmW, &full_bar[i], (kb0 + i) * kBK, n0);
+    }
+    grid_wait();
+    for (int i = 0; i < pre; ++i) {
+      uint8_t* sx = base + (size_t)i * kStageBytes + kWStageBytes;
+      tma_load_2d(sx, &tmX, &full_bar[i], (kb0 + i) * kBK, m0);
+    }
+    for (int i = pre; i < nkb; ++i) {
       const int s = i % stages;
       const uint32_t ph = (uint32_t)(i / stages) & 1u;
       mbar_wait(&empty_bar[s], ph ^ 1u);
@@ -146,6 +161,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 
   // ---------------- epilogue: TMEM -> fp32 partials ----------------
+  grid_wait();  // the predecessor may still read the partial buffer
   if (nkb > 0) {
     mbar_wait(&done_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -264,11 +280,18 @@ static cudaError_t launch_nt(const TcGemmArgs& a, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((a.N + kWRows - 1) / kWRows, (a.M + NT - 1) / NT, a.splits);
-  gemm_tc_kernel<NT><<<grid, kTcThreads, smem, stream>>>(
-      *(const CUtensorMap*)a.tmW, *(const CUtensorMap*)a.tmX, a.C, a.M, a.N, a.K / kBK, a.splits,
-      stages);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.N + kWRows - 1) / kWRows, (a.M + NT - 1) / NT, a.splits);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<NT>, *(const CUtensorMap*)a.tmW,
+                            *(const CUtensorMap*)a.tmX, a.C, a.M, a.N, a.K / kBK, a.splits, stages);
 }
 
 cudaError_t gemm_tc_launch(const TcGemmArgs& a, cudaStream_t stream) {

@@ -90,6 +90,7 @@ struct AttnParams {
   unsigned int* counters;    // [M, KV]
   int layer, n_pages, n_heads, n_kv, nsplit;
   int start_pos;             // prefill: position of row 0
+  int sep_merge;             // prefill: leave split partials for attn_merge_launch
   DecodeState* st;           // decode: ctx_len / page table from here
 };
 
@@ -101,6 +102,7 @@ cudaError_t attn_decode_tc_launch(const AttnParams& p, cudaStream_t stream, bool
 cudaError_t attn_tc_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream,
                            bool pdl);
 int attn_tc_splits(int n_kv, int q_tiles, int T, int num_sms);
+cudaError_t attn_merge_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream);
 cudaError_t attn_prefill_launch(const AttnParams& p, int M, cudaStream_t stream);
 
 // ----------------------------------------------------------- prefill path ---

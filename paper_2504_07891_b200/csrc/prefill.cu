@@ -150,6 +150,25 @@ cudaError_t gemm_launch(const GemmParams& p, cudaStream_t stream) {
 
 // ========================================================= epilogues ======
 constexpr int kEpiThreads = 256;
+constexpr int kEpiRowThreads = 1024;  // one CTA per token row: wide, for latency
+
+// launch with programmatic dependent launch: the kernel starts while its
+// predecessor drains and calls grid_wait() before touching its outputs
+template <typename... Args, typename... Actual>
+static cudaError_t launch_pdl(void (*fn)(Args...), dim3 grid, int block, size_t smem,
+                              cudaStream_t stream, Actual... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, args...);
+}
 
 // h[m] = embed[ids[m]];  x[m] = bf16(rmsnorm(h[m]) * w)
 __global__ void embed_norm_kernel(const int* ids, const __nv_bfloat16* embed, int d,
@@ -176,14 +195,22 @@ cudaError_t embed_norm_launch(const int* ids, int M, const __nv_bfloat16* embed,
   return cudaGetLastError();
 }
 
+// fixed-order sum of the split-K partials; the (<= 8) loads are independent
+// predicated loads, so they are all in flight together
 SR_DEV float sum_splits(const float* part, int splits, size_t stride, size_t idx) {
+  float a[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) a[s] = s < splits ? __ldcg(part + s * stride + idx) : 0.f;
   float v = 0.f;
-  for (int s = 0; s < splits; ++s) v += part[s * stride + idx];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v += a[s];
   return v;
 }
 
 // q/k: bias + RoPE (pairs j, j+64); k, v -> pages; q -> bf16 buffer
 __global__ void epi_qkv_kernel(EpiParams p) {
+  grid_launch_dependents();
+  grid_wait();
   const int m = blockIdx.x;
   const int pos = p.start_pos + m;
   const size_t stride = (size_t)p.M * p.N;
@@ -220,12 +247,13 @@ __global__ void epi_qkv_kernel(EpiParams p) {
 }
 
 cudaError_t epi_qkv_launch(const EpiParams& p, cudaStream_t stream) {
-  epi_qkv_kernel<<<p.M, kEpiThreads, 0, stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(epi_qkv_kernel, dim3(p.M), kEpiRowThreads, 0, stream, p);
 }
 
 // h[m] += sum_s part;  x[m] = bf16(rmsnorm(h[m]) * w)   (N == d)
 __global__ void epi_resid_norm_kernel(EpiParams p) {
+  grid_launch_dependents();
+  grid_wait();
   extern __shared__ float hrow[];
   __shared__ float red[32];
   const int m = blockIdx.x, d = p.N;
@@ -244,12 +272,13 @@ __global__ void epi_resid_norm_kernel(EpiParams p) {
 }
 
 cudaError_t epi_resid_norm_launch(const EpiParams& p, cudaStream_t stream) {
-  epi_resid_norm_kernel<<<p.M, kEpiThreads, p.N * sizeof(float), stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(epi_resid_norm_kernel, dim3(p.M), kEpiRowThreads, p.N * sizeof(float), stream, p);
 }
 
 // act[m][u] = bf16(silu(gate) * up) from interleaved 16-row blocks
 __global__ void epi_glu_kernel(EpiParams p) {
+  grid_launch_dependents();
+  grid_wait();
   const int m = blockIdx.y;
   const int f = p.N / 2;
   const size_t stride = (size_t)p.M * p.N;
@@ -264,8 +293,7 @@ __global__ void epi_glu_kernel(EpiParams p) {
 cudaError_t epi_glu_launch(const EpiParams& p, cudaStream_t stream) {
   const int f = p.N / 2;
   dim3 grid((f + kEpiThreads - 1) / kEpiThreads, p.M);
-  epi_glu_kernel<<<grid, kEpiThreads, 0, stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(epi_glu_kernel, grid, kEpiThreads, 0, stream, p);
 }
 
 // ======================================================= verify readout ====

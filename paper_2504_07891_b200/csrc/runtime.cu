@@ -438,7 +438,9 @@ struct Model {
           const int G = d.n_heads / d.n_kv_heads;
           const int q_tiles = (M * G + 63) / 64;
           a.nsplit = std::min(kAttnPrefillSplit, attn_tc_splits(d.n_kv_heads, q_tiles, Tlast, num_sms));
-          SR_CK(attn_tc_launch(a, M, a.nsplit, s, false));
+          a.sep_merge = 1;
+          SR_CK(attn_tc_launch(a, M, a.nsplit, s, true));
+          if (a.nsplit > 1) SR_CK(attn_merge_launch(a, M, a.nsplit, s));
           watch(s, "attn_prefill_tc", l, M, a.nsplit);
         }
         // o-proj + residual + norm2

@@ -1,4 +1,5 @@
-timeout 300 python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -2
-for m in r1-1.5b qwen2.5-7b; do
-timeout 300 python tools/mk_prof.py $m --ctx 2048 > gpurun_out/mkprof_$m.log 2>&1
-done
+timeout 300 python tools/verify_profile.py qwen2.5-7b --ctx 2048 --m 80 > gpurun_out/vp7b.log 2>&1
+timeout 300 python tools/verify_profile.py r1-1.5b --ctx 2048 --m 80 > gpurun_out/vp15b.log 2>&1
+timeout 300 python tools/verify_profile.py qwen2.5-7b --ctx 2048 --m 640 > gpurun_out/vp7b640.log 2>&1
+cat gpurun_out/vp7b.log gpurun_out/vp15b.log gpurun_out/vp7b640.log
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
