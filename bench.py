@@ -175,12 +175,18 @@ def run_ours(args) -> None:
 
     dist, rank, world, local = _dist()
     torch.cuda.set_device(local)
+    base_tp = None
+    if args.mode == "tp":  # config C4: base sharded over the ranks, one shared trajectory
+        from paper_2504_07891_b200.backend import TensorParallel
+
+        base_tp = TensorParallel.from_dist() if dist is not None else TensorParallel.single()
     small, base = build_pair(args.pair, seed=args.seed, max_ctx=args.budget + 512,
-                             threshold=args.threshold)
+                             threshold=args.threshold, base_tp=base_tp)
     vocab = shared_vocab(get_spec(PAIRS[args.pair][0]).vocab_text)
     cfg = EngineConfig(threshold=AcceptanceThreshold(args.threshold), temperature=0.0,
                        token_budget=args.budget, max_step_tokens=args.max_step_tokens)
-    problems = [rank * 1000 + i for i in range(64)]
+    # DP: independent problems per rank; TP: every rank drives the same one
+    problems = [(0 if args.mode == "tp" else rank) * 1000 + i for i in range(64)]
     src = StepSource(small, base, cfg, problems, vocab)
 
     for _ in range(args.warmup):
@@ -210,7 +216,7 @@ def run_ours(args) -> None:
     lat = [o.step.latency for o in outcomes]
     n_spec = sum(1 for o in outcomes if o.action.value == "AcceptedSpeculation")
 
-    tot_tokens = _reduce_sum(dist, tokens)
+    tot_tokens = _reduce_sum(dist, tokens) if args.mode == "dp" else tokens
     max_dev_ms = _reduce_max(dist, dev_ms)
     max_wall_ms = _reduce_max(dist, wall_ms)
     peaks = _peaks()
@@ -229,13 +235,15 @@ def run_ours(args) -> None:
         "warmup": args.warmup,
         "ms_per_step": round(max_wall_ms / args.steps, 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if args.mode == "dp" else "strong",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights, seeded 64-word problems)",
         "config": {"workload": WORKLOADS[args.pair], "pair": args.pair, "threshold": args.threshold,
                    "token_budget": args.budget, "max_step_tokens": args.max_step_tokens,
-                   "batch": 1, "parallelism": f"dp{world} (independent problems per GPU)",
+                   "batch": 1, "parallelism": (f"dp{world} (independent problems per GPU)"
+                                               if args.mode == "dp" else
+                                               f"tp{world} (base sharded, NCCL all-reduce; draft replicated)"),
                    "l2": "weights (17 GB) exceed L2 (126 MB): no flush needed"},
         "e2e": {"value": round(tot_tokens / (max_wall_ms * 1e-3), 2), "unit": UNIT,
                 "ms_per_step": round(max_wall_ms / args.steps, 3),
@@ -438,6 +446,9 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="dp", choices=["dp", "tp"],
+                    help="multi-GPU: dp = independent problems per rank (C5), "
+                         "tp = base model tensor-parallel over the ranks (C4)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

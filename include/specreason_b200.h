@@ -54,6 +54,7 @@ extern "C" {
 #define SR_E_INVALID 1001     /* bad descriptor / argument */
 #define SR_E_CAPACITY 1002    /* request exceeds a compiled or declared limit */
 #define SR_E_GRAPH 1003       /* CUDA graph construction failed */
+#define SR_E_TP 1004          /* NCCL unavailable or a collective failed */
 
 /* finish codes written to sr_generate's output */
 #define SR_FINISH_LENGTH 0
@@ -80,6 +81,12 @@ typedef struct sr_model_desc {
   int32_t max_tokens;   /* largest n_ids of one prefill call */
   int32_t max_new;      /* largest max_new of one sr_generate call */
   int32_t n_pages;      /* pages in each of the K and V pools */
+  /* tensor parallelism (1 = off).  The caller passes this rank's shard
+   * (heads, ffn units and LM-head rows divided by tp_world; embedding and
+   * norms whole) and attaches a communicator with sr_model_set_tp. */
+  int32_t tp_world;
+  int32_t tp_rank;
+  int32_t vocab_base;   /* global token id of LM-head row 0 of this shard */
 } sr_model_desc;
 
 typedef struct sr_layer_ptrs {
@@ -159,6 +166,19 @@ int sr_score(void* model, const int32_t* page_table, int32_t start_pos,
 int sr_forward_logits(void* model, const int32_t* page_table, int32_t start_pos,
                       const int32_t* ids, int32_t n_ids, int32_t all, float* logits,
                       void* stream);
+
+/*
+ * Tensor parallelism over NCCL (loaded with dlopen on first use).  Rank 0
+ * creates the 128-byte id, the caller distributes it, every rank creates its
+ * communicator and attaches it to its model.  With a communicator attached,
+ * O and down partial outputs are all-reduced (fp32 sum) before the residual
+ * add, greedy choices merge an all-gathered (top-1, index, top-2) per rank,
+ * and the judge readout all-reduces the ten digit rank counts.
+ */
+int sr_tp_unique_id(uint8_t* h_id128);
+int sr_tp_comm_create(const uint8_t* h_id128, int32_t world, int32_t rank, void** out_comm);
+int sr_tp_comm_destroy(void* comm);
+int sr_model_set_tp(void* model, void* comm);
 
 /* device timings of the last sr_generate / sr_score on this model */
 int sr_last_timing(void* model, sr_timing* h_out);

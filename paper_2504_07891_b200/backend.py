@@ -26,7 +26,8 @@ import torch
 from . import native
 from .domain import BackendProfile, BackendRole
 from .host import ModelBackend, Readout, Stream
-from .shapes import PAIRS, ModelSpec, get_spec, make_weights, rope_table, tensor_shapes
+from .shapes import (PAIRS, ModelSpec, get_spec, make_tp_weights, make_weights, rope_table,
+                     shard_weights, tensor_shapes, tp_spec)
 from .vocab import Vocab, shared_vocab
 
 PAGE = native.SR_PAGE
@@ -67,7 +68,8 @@ class DeviceModel:
             n_layers=spec.n_layers, d_model=spec.d_model, n_heads=spec.n_heads,
             n_kv_heads=spec.n_kv_heads, head_dim=spec.head_dim, d_ffn=spec.d_ffn,
             vocab_rows=spec.vocab_rows, vocab_text=spec.vocab_text, rms_eps=spec.rms_eps,
-            max_pos=max_pos, max_tokens=max_tokens, max_new=max_new, n_pages=n_pages)
+            max_pos=max_pos, max_tokens=max_tokens, max_new=max_new, n_pages=n_pages,
+            tp_world=spec.tp_world, tp_rank=spec.tp_rank, vocab_base=spec.vocab_base)
         ws = self.lib.sr_workspace_bytes(C.byref(self.desc))
         if ws == 0:
             raise native.NativeError("sr_workspace_bytes", -1, self.lib.sr_last_error().decode())
@@ -194,7 +196,9 @@ class NativeEngine:
         self.vocab = vocab
         self.streams: list[Stream] = []
         self._classes: dict[tuple[str, ...], torch.Tensor] = {}
-        self.first_digit = first_digit_table(vocab, model.spec.vocab_rows).to(model.device)
+        # token-indexed tables span the global vocabulary (the embedding rows)
+        self.n_ids = model.spec.embed_rows or model.spec.vocab_rows
+        self.first_digit = first_digit_table(vocab, self.n_ids).to(model.device)
         self.max_pages = math.ceil(model.max_pos / PAGE)
         self.last_margins: list[float] = []
         self.stats = EngineStats()
@@ -240,7 +244,7 @@ class NativeEngine:
     def _class_table(self, stop: tuple[str, ...]) -> torch.Tensor:
         t = self._classes.get(stop)
         if t is None:
-            cls = self.vocab.token_classes(stop, self.spec.vocab_rows)
+            cls = self.vocab.token_classes(stop, self.n_ids)
             t = torch.from_numpy(cls.copy()).to(self.model.device)
             self._classes[stop] = t
         return t
@@ -305,6 +309,45 @@ class NativeEngine:
         return out
 
 
+class TensorParallel:
+    """An NCCL communicator of the C-ABI (``sr_tp_comm_create``) for one rank
+    of a tensor-parallel base model.  ``from_dist`` distributes the 128-byte
+    id over an initialised torch.distributed group (gloo or nccl)."""
+
+    def __init__(self, rank: int, world: int, uid: bytes) -> None:
+        lib = native.load()
+        self.rank, self.world = rank, world
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        comm = C.c_void_p()
+        native.check("sr_tp_comm_create", lib.sr_tp_comm_create(buf, world, rank, C.byref(comm)))
+        self.comm = comm
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        native.check("sr_tp_unique_id", native.load().sr_tp_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_dist(cls, group=None) -> "TensorParallel":
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        return cls(rank, world, box[0])
+
+    @classmethod
+    def single(cls) -> "TensorParallel":
+        """World-size-1 communicator: runs every TP code path on one GPU."""
+        return cls(0, 1, cls.unique_id())
+
+    def close(self) -> None:
+        if self.comm is not None and self.comm.value:
+            native.load().sr_tp_comm_destroy(self.comm)
+            self.comm = None
+
+
 class B200Backend(ModelBackend):
     """Drop-in ``Backend`` whose model runs on the B200 (see module doc)."""
 
@@ -312,17 +355,29 @@ class B200Backend(ModelBackend):
                  weights: dict[str, torch.Tensor] | None = None, max_ctx: int = 8192,
                  n_streams: int = 4, threshold: int = 7, max_new: int = 256,
                  max_tokens: int = 256, device: str = "cuda", init_device: str | None = None,
-                 vocab: Vocab | None = None, types=None, record: bool = False) -> None:
+                 vocab: Vocab | None = None, types=None, record: bool = False,
+                 tp: "TensorParallel | None" = None) -> None:
         if not torch.cuda.is_available():
             raise RuntimeError("B200Backend needs a CUDA device (no CPU fallback)")
         spec = get_spec(spec) if isinstance(spec, str) else spec
+        full_spec = spec
+        if tp is not None:  # this rank's shard of the model (config C4)
+            spec = tp_spec(full_spec, tp.rank, tp.world)
         if weights is None:
             init_device = init_device or ("cpu" if spec.d_model <= 512 else device)
-            weights = make_weights(spec, seed, device=init_device)
+            if tp is not None:
+                weights = make_tp_weights(full_spec, tp.rank, tp.world, seed, device=init_device)
+            else:
+                weights = make_weights(spec, seed, device=init_device)
+        elif tp is not None and tuple(weights["lm_head"].shape)[0] == full_spec.vocab_rows:
+            weights = shard_weights(weights, full_spec, tp.rank, tp.world)
         max_pos = max_ctx + max_new + 64
         pages_per_stream = math.ceil(max_pos / PAGE) + 1
         model = DeviceModel(spec, weights, max_pos=max_pos, n_pages=n_streams * pages_per_stream,
                             max_tokens=max_tokens, max_new=max_new, device=device)
+        if tp is not None:
+            native.check("sr_model_set_tp", model.lib.sr_model_set_tp(model.handle, tp.comm))
+        self.tp = tp
         vocab = vocab or shared_vocab(spec.vocab_text)
         T = types
         prof_cls = T.BackendProfile if T else BackendProfile
@@ -336,11 +391,14 @@ class B200Backend(ModelBackend):
 
 
 def build_pair(pair: str = "tiny", *, seed: int = 0, max_ctx: int = 8192, threshold: int = 7,
-               types=None, record: bool = False, **kw) -> tuple[B200Backend, B200Backend]:
-    """(small, base) backends for a named model pair (``shapes.PAIRS``)."""
+               types=None, record: bool = False, base_tp: TensorParallel | None = None,
+               **kw) -> tuple[B200Backend, B200Backend]:
+    """(small, base) backends for a named model pair (``shapes.PAIRS``).
+    With ``base_tp`` the base model is this rank's tensor-parallel shard and
+    the draft is replicated (SPMD: every rank drives the same trajectory)."""
     small_name, base_name = PAIRS[pair]
     small = B200Backend(small_name, BackendRole.SMALL, seed=seed, max_ctx=max_ctx,
                         threshold=threshold, types=types, record=record, **kw)
     base = B200Backend(base_name, BackendRole.BASE, seed=seed, max_ctx=max_ctx,
-                       threshold=threshold, types=types, record=record, **kw)
+                       threshold=threshold, types=types, record=record, tp=base_tp, **kw)
     return small, base

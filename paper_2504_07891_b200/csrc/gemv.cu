@@ -375,7 +375,7 @@ static int pick_ks(int rows, int K, int num_sms) {
 
 cudaError_t gemv_launch(GemvKind kind, GemvParams p, int num_sms, cudaStream_t stream, bool pdl) {
   if (p.K > 5120 && (kind == GEMV_QKV || kind == GEMV_QKV_EMBED || kind == GEMV_GLU ||
-                     kind == GEMV_LM_ARGMAX))
+                     kind == GEMV_LM_ARGMAX || kind == GEMV_LM_LOGITS))
     return cudaErrorInvalidValue;  // RMSNorm prologue keeps d <= 5120 values in registers
   switch (kind) {
     case GEMV_QKV_EMBED:
@@ -404,6 +404,9 @@ cudaError_t gemv_launch(GemvKind kind, GemvParams p, int num_sms, cudaStream_t s
     case GEMV_LM_LOGITS_X:
       p.n_tasks = (p.N + 1) / 2;
       return launch1<IN_X, EPI_LOGITS, 2, 4>(p, num_sms, stream, pdl);
+    case GEMV_LM_LOGITS:
+      p.n_tasks = (p.N + 1) / 2;
+      return launch1<IN_H_NORM, EPI_LOGITS, 2, 4>(p, num_sms, stream, pdl);
   }
   return cudaErrorInvalidValue;
 }

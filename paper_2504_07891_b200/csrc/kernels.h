@@ -16,6 +16,7 @@ enum GemvKind {
   GEMV_LM_ARGMAX,   // RMSNorm(h) -> logits -> greedy token (+ stop test)
   GEMV_LM_ARGMAX_X, // normalised x -> logits -> greedy token
   GEMV_LM_LOGITS_X, // normalised x -> fp32 logits
+  GEMV_LM_LOGITS,   // RMSNorm(h) -> fp32 logits (vocab-parallel decode)
 };
 
 struct GemvParams {
@@ -219,6 +220,31 @@ int mk_max_j(int N, int K, int num_sms);
 int mk_tile_rows();
 int mk_tile_cols();
 cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream);
+
+// tensor parallelism (tp.cu)
+int tp_available();
+const char* tp_error_string(int code);
+int tp_unique_id(void* out128);
+int tp_comm_create(const void* id128, int world, int rank, void** out);
+int tp_comm_destroy(void* comm);
+int tp_all_reduce_f32(void* comm, float* buf, size_t n, cudaStream_t s);
+int tp_all_reduce_i32(void* comm, int* buf, size_t n, cudaStream_t s);
+int tp_all_gather_f32(void* comm, const float* send, float* recv, size_t n, cudaStream_t s);
+int tp_broadcast_f32(void* comm, const float* send, float* recv, size_t n, int root,
+                     cudaStream_t s);
+cudaError_t split_sum_launch(const float* part, int splits, size_t stride, float* delta, size_t n,
+                             cudaStream_t s);
+cudaError_t add_delta_launch(float* h, float* delta, int n, cudaStream_t s);
+cudaError_t tp_top2_local_launch(const float* logits, int n_valid, int base, float* pv1,
+                                 float* pv2, int* pi1, unsigned* counter, float* send, int grid,
+                                 cudaStream_t s);
+cudaError_t tp_select_launch(const float* gathered, int world, DecodeState* st, cudaStream_t s);
+cudaError_t tp_readout_local_launch(const float* logits, int n_valid, int base, const float* dig,
+                                    int* counts, float* pv1, float* pv2, int* pi1,
+                                    unsigned* counter, float* send, int grid, cudaStream_t s);
+cudaError_t tp_readout_final_launch(const float* dig, int* counts, const float* gathered,
+                                    int world, const int8_t* first_digit, int threshold,
+                                    sr_readout* out, cudaStream_t s);
 
 // decode-loop bookkeeping kernels
 cudaError_t decode_begin_launch(DecodeState* st, const DecodeState* h_init, cudaStream_t stream);

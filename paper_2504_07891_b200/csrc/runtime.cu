@@ -44,7 +44,8 @@ constexpr int kAttnPrefillSplit = 16;
 
 struct Layout {  // workspace carve-up (byte offsets)
   size_t st, h, x, q, attn, act, part, apart, actr, lm_v1, lm_v2, lm_i1, lm_ctr, logits, ro_cnt,
-      mk_maps, mk_layers, mk_h, mk_part, mk_apart, mk_lm, mk_prof, mk_ctab, total;
+      mk_maps, mk_layers, mk_h, mk_part, mk_apart, mk_lm, mk_prof, mk_ctab, tp_delta, tp_small,
+      total;
   int mk_maxj;
   int nsplit_decode;
   size_t part_floats;
@@ -91,6 +92,9 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
   L.mk_lm = take((size_t)num_sms * 3 * 4);
   L.mk_prof = take((size_t)SR_PROF_EVENTS * 8);
   L.mk_ctab = take(3 * 256 * 2 + 64 * 4);
+  // tensor parallelism: the all-reduced row-parallel output, exchange buffers
+  L.tp_delta = take(T * d.d_model * 4);
+  L.tp_small = take(4096 + 4 * 8192);  // exchange words + the decode delta row
   L.total = o;
   return L;
 }
@@ -123,6 +127,10 @@ struct Model {
   bool graph_decode = false;   // SR_DECODE=graph: per-kernel decode graph (A/B reference)
   MkParams mk{};
   int* trace_host = nullptr;
+  void* tp_comm = nullptr;  // sr_model_set_tp; non-null: the TP code paths run
+  float* tp_delta = nullptr;
+  float *tp_send, *tp_gather, *tp_dig, *tp_dec;
+  int* tp_counts;
   bool attn_simt = false;      // SR_ATTN=simt: CUDA-core split-KV attention (A/B reference)
   bool prefetch = false;       // SR_PREFETCH=1: GEMV L2 prefetch before the PDL wait
   struct alignas(64) TMap { CUtensorMap m; };
@@ -448,6 +456,8 @@ struct Model {
         if (rc) return -rc;
         ep = epi_base(M, d.d_model);
         ep.norm_w = lw(l, LN2);
+        if (tp_comm)
+          if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
         SR_CK(epi_resid_norm_launch(ep, s));
         // gate/up
         rc = gemm(ACT_X, l * 4 + 2, x, lw(l, WGU), M, 2 * d.d_ffn, d.d_model, s);
@@ -460,11 +470,105 @@ struct Model {
         if (rc) return -rc;
         ep = epi_base(M, d.d_model);
         ep.norm_w = (l + 1 < d.n_layers) ? lw(l + 1, LN1) : ln_f;
+        if (tp_comm)
+          if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
         SR_CK(epi_resid_norm_launch(ep, s));
       }
     }
     *last_rows = rows;
     return 0;
+  }
+
+  // ----------------------------------------------------- tensor parallel ---
+  int tp_check(int r, const char* what) {
+    if (r != 0) return fail(SR_E_TP, std::string(what) + ": " + tp_error_string(r));
+    return 0;
+  }
+
+  // prefill: all-reduce the row-parallel output (split partials -> delta)
+  // and point the residual epilogue at it
+  int tp_reduce_rows(EpiParams& ep, int M, cudaStream_t s) {
+    const size_t n = (size_t)M * d.d_model;
+    SR_CK(split_sum_launch(part, ep.splits, (size_t)M * d.d_model, tp_delta, n, s));
+    if (int rc = tp_check(tp_all_reduce_f32(tp_comm, tp_delta, n, s), "ncclAllReduce")) return rc;
+    ep.part = tp_delta;
+    ep.splits = 1;
+    return 0;
+  }
+
+  // greedy step over vocab-parallel logits (local rows in `logits`)
+  int tp_select(cudaStream_t s) {
+    const int grid = std::min(gemv_max_grid(num_sms), (d.vocab_text + 255) / 256);
+    SR_CK(tp_top2_local_launch(logits, d.vocab_text, d.vocab_base, lm_v1, lm_v2, lm_i1, lm_ctr,
+                               tp_send, std::max(grid, 1), s));
+    if (int rc = tp_check(tp_all_gather_f32(tp_comm, tp_send, tp_gather, 3, s), "ncclAllGather"))
+      return rc;
+    SR_CK(tp_select_launch(tp_gather, d.tp_world, st, s));
+    return 0;
+  }
+
+  // one decoded token with the TP exchanges (host-driven loop)
+  int tp_decode_step(cudaStream_t s) {
+    for (int l = 0; l < d.n_layers; ++l) {
+      GemvParams p = gemv_base();
+      p.layer = l;
+      p.W = lw(l, WQKV);
+      p.N = qkv_rows;
+      p.K = d.d_model;
+      p.norm_w = lw(l, LN1);
+      p.bias = lw(l, BQKV);
+      p.embed = embed;
+      p.qout = q;
+      SR_CK(gemv_launch(l == 0 ? GEMV_QKV_EMBED : GEMV_QKV, p, num_sms, s, false));
+      AttnParams a{};
+      a.q = q;
+      a.out = attn;
+      a.k_pool = k_pool;
+      a.v_pool = v_pool;
+      a.part = apart;
+      a.counters = actr;
+      a.layer = l;
+      a.n_pages = d.n_pages;
+      a.n_heads = d.n_heads;
+      a.n_kv = d.n_kv_heads;
+      a.nsplit = L.nsplit_decode;
+      a.st = st;
+      SR_CK(attn_decode_tc_launch(a, s, false));
+      for (int half = 0; half < 2; ++half) {
+        p = gemv_base();
+        if (half == 0) {  // o-proj (row parallel) -> delta
+          p.W = lw(l, WO);
+          p.N = d.d_model;
+          p.K = q_dim;
+          p.x = attn;
+        } else {          // gate/up, then down (row parallel) -> delta
+          GemvParams g = gemv_base();
+          g.W = lw(l, WGU);
+          g.N = 2 * d.d_ffn;
+          g.K = d.d_model;
+          g.norm_w = lw(l, LN2);
+          g.act_out = act;
+          SR_CK(gemv_launch(GEMV_GLU, g, num_sms, s, false));
+          p.W = lw(l, WD);
+          p.N = d.d_model;
+          p.K = d.d_ffn;
+          p.x = act;
+        }
+        p.h = tp_dec;  // zero on entry; the residual GEMV adds into it
+        SR_CK(gemv_launch(GEMV_RESID, p, num_sms, s, false));
+        if (int rc = tp_check(tp_all_reduce_f32(tp_comm, tp_dec, d.d_model, s), "ncclAllReduce"))
+          return rc;
+        SR_CK(add_delta_launch(h, tp_dec, d.d_model, s));
+      }
+    }
+    GemvParams p = gemv_base();
+    p.W = lm_head;
+    p.N = d.vocab_rows;
+    p.K = d.d_model;
+    p.norm_w = ln_f;
+    p.logits = logits;
+    SR_CK(gemv_launch(GEMV_LM_LOGITS, p, num_sms, s, false));
+    return tp_select(s);
   }
 
   int last_splits = 1;
@@ -557,6 +661,8 @@ static int validate(const sr_model_desc* d) {
     return fail(SR_E_INVALID, "vocab sizes must be even, text <= rows");
   if (d->max_tokens < 1 || d->max_new < 1 || d->n_pages < 1 || d->max_pos < 1)
     return fail(SR_E_INVALID, "capacities must be positive");
+  if (d->tp_world < 1 || d->tp_rank < 0 || d->tp_rank >= d->tp_world || d->vocab_base < 0)
+    return fail(SR_E_INVALID, "bad tensor-parallel fields");
   return 0;
 }
 
@@ -617,6 +723,12 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
   m->lm_ctr = m->at<unsigned>(m->L.lm_ctr);
   m->logits = m->at<float>(m->L.logits);
   m->ro_cnt = m->at<unsigned>(m->L.ro_cnt);
+  m->tp_delta = m->at<float>(m->L.tp_delta);
+  m->tp_send = m->at<float>(m->L.tp_small);
+  m->tp_dig = m->tp_send + 16;
+  m->tp_counts = reinterpret_cast<int*>(m->tp_send + 32);
+  m->tp_gather = m->tp_send + 64;  // [world][3], world <= 64
+  m->tp_dec = m->tp_send + 1024;   // decode delta row (zero between uses)
   cudaStream_t s = (cudaStream_t)stream;
   // zero the whole workspace once: counters must start at 0
   cudaError_t e = cudaMemsetAsync(m->ws, 0, m->L.total, s);
@@ -674,6 +786,7 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
   if (!m || !page_table || !ids || !token_class || !out) return fail(SR_E_INVALID, "null argument");
   if (n_ids < 1 || max_new < 1 || start_pos < 0) return fail(SR_E_INVALID, "bad sizes");
   if (max_new > m->d.max_new) return fail(SR_E_CAPACITY, "max_new exceeds the model's max_new");
+  if (m->d.tp_world > 1 && !m->tp_comm) return fail(SR_E_INVALID, "tensor-parallel model without a communicator");
   if (start_pos + n_ids + max_new > m->d.max_pos)
     return fail(SR_E_CAPACITY, "positions exceed max_pos");
   cudaStream_t s = (cudaStream_t)stream;
@@ -703,9 +816,24 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
   p.part_v2 = m->lm_v2;
   p.part_i1 = m->lm_i1;
   p.counter = m->lm_ctr;
-  SR_CK(gemv_launch(GEMV_LM_ARGMAX_X, p, m->num_sms, s, false));
+  if (m->tp_comm) {  // vocab-parallel first choice
+    p.logits = m->logits;
+    SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
+    if (int rc2 = m->tp_select(s)) return rc2;
+  } else {
+    SR_CK(gemv_launch(GEMV_LM_ARGMAX_X, p, m->num_sms, s, false));
+  }
   SR_CK(cudaEventRecord(m->ev[1], s));
-  if (!m->stream_decode && !m->graph_decode) {
+  if (m->tp_comm) {
+    // host-driven token loop: the exchanges are NCCL calls between kernels
+    for (int i = 0; i < max_new; ++i) {
+      int done = 0;
+      SR_CK(cudaMemcpyAsync(&done, &m->st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SR_CK(cudaStreamSynchronize(s));
+      if (done) break;
+      if (int rc2 = m->tp_decode_step(s)) return rc2;
+    }
+  } else if (!m->stream_decode && !m->graph_decode) {
     // one persistent kernel decodes the whole step (decode_mk.cu)
     SR_CK(mk_launch(m->mk, m->num_sms, s));
   } else if (m->graph_decode) {
@@ -735,6 +863,7 @@ int sr_score(void* model, const int32_t* page_table, int32_t start_pos, const in
   if (!m || !page_table || !ids || !first_digit || !readout) return fail(SR_E_INVALID, "null argument");
   if (n_ids < 1 || start_pos < 0) return fail(SR_E_INVALID, "bad sizes");
   if (start_pos + n_ids > m->d.max_pos) return fail(SR_E_CAPACITY, "positions exceed max_pos");
+  if (m->d.tp_world > 1 && !m->tp_comm) return fail(SR_E_INVALID, "tensor-parallel model without a communicator");
   cudaStream_t s = (cudaStream_t)stream;
   SR_CK(cudaEventRecord(m->ev[0], s));
   int rows = 0;
@@ -748,6 +877,29 @@ int sr_score(void* model, const int32_t* page_table, int32_t start_pos, const in
   p.x = m->x + (size_t)(rows - 1) * m->d.d_model;
   p.logits = m->logits;
   SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
+  if (m->tp_comm) {
+    // digits 0-9 are rows of rank 0's shard: broadcast their logits, count
+    // ranks locally, all-reduce the counts, all-gather the local top-2s
+    if (int rc2 = m->tp_check(tp_broadcast_f32(m->tp_comm, m->logits, m->tp_dig, 10, 0, s),
+                              "ncclBroadcast"))
+      return rc2;
+    const int grid = std::max(1, std::min(m->num_sms, (m->d.vocab_text + 255) / 256));
+    SR_CK(tp_readout_local_launch(m->logits, m->d.vocab_text, m->d.vocab_base, m->tp_dig,
+                                  m->tp_counts, m->lm_v1, m->lm_v2, m->lm_i1, m->lm_ctr,
+                                  m->tp_send, grid, s));
+    if (int rc2 = m->tp_check(tp_all_reduce_i32(m->tp_comm, m->tp_counts, 10, s), "ncclAllReduce"))
+      return rc2;
+    if (int rc2 = m->tp_check(tp_all_gather_f32(m->tp_comm, m->tp_send, m->tp_gather, 3, s),
+                              "ncclAllGather"))
+      return rc2;
+    SR_CK(tp_readout_final_launch(m->tp_dig, m->tp_counts, m->tp_gather, m->d.tp_world,
+                                  first_digit, threshold, readout, s));
+    SR_CK(cudaEventRecord(m->ev[1], s));
+    SR_CK(cudaEventRecord(m->ev[2], s));
+    m->timing.prefill_tokens = n_ids;
+    m->timing.decode_tokens = 0;
+    return 0;
+  }
   ReadoutParams r{};
   r.logits = m->logits;
   r.n_valid = m->d.vocab_text;
@@ -801,6 +953,34 @@ int sr_forward_logits(void* model, const int32_t* page_table, int32_t start_pos,
       SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
     }
   }
+  return 0;
+}
+
+int sr_tp_unique_id(uint8_t* h_id128) {
+  if (!h_id128) return fail(SR_E_INVALID, "null argument");
+  if (!tp_available()) return fail(SR_E_TP, "libnccl.so.2 not loadable");
+  const int r = tp_unique_id(h_id128);
+  return r ? fail(SR_E_TP, std::string("ncclGetUniqueId: ") + tp_error_string(r)) : 0;
+}
+
+int sr_tp_comm_create(const uint8_t* h_id128, int32_t world, int32_t rank, void** out_comm) {
+  if (!h_id128 || !out_comm || world < 1 || world > 64 || rank < 0 || rank >= world)
+    return fail(SR_E_INVALID, "bad communicator arguments");
+  if (!tp_available()) return fail(SR_E_TP, "libnccl.so.2 not loadable");
+  const int r = tp_comm_create(h_id128, world, rank, out_comm);
+  return r ? fail(SR_E_TP, std::string("ncclCommInitRank: ") + tp_error_string(r)) : 0;
+}
+
+int sr_tp_comm_destroy(void* comm) {
+  const int r = tp_comm_destroy(comm);
+  return r ? fail(SR_E_TP, std::string("ncclCommDestroy: ") + tp_error_string(r)) : 0;
+}
+
+int sr_model_set_tp(void* model, void* comm) {
+  Model* m = (Model*)model;
+  if (!m) return fail(SR_E_INVALID, "null model");
+  if (m->d.tp_world > 1 && !comm) return fail(SR_E_INVALID, "tp_world > 1 needs a communicator");
+  m->tp_comm = comm;
   return 0;
 }
 

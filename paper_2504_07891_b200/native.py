@@ -19,7 +19,8 @@ class ModelDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn",
         "vocab_rows", "vocab_text")] + [("rms_eps", C.c_float)] + [
-        (n, C.c_int32) for n in ("max_pos", "max_tokens", "max_new", "n_pages")]
+        (n, C.c_int32) for n in ("max_pos", "max_tokens", "max_new", "n_pages", "tp_world",
+                                 "tp_rank", "vocab_base")]
 
 
 class LayerPtrs(C.Structure):
@@ -58,6 +59,10 @@ EXPORTS = {
     "sr_last_timing": (C.c_int, [C.c_void_p, C.POINTER(Timing)]),
     "sr_debug_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "sr_debug_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "sr_tp_unique_id": (C.c_int, [C.c_void_p]),
+    "sr_tp_comm_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "sr_tp_comm_destroy": (C.c_int, [C.c_void_p]),
+    "sr_model_set_tp": (C.c_int, [C.c_void_p, C.c_void_p]),
 }
 
 _lib = None

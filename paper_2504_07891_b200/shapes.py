@@ -62,6 +62,11 @@ class ModelSpec:
     digit_gain: float = 6.0
     digit_noise: float = 1.0
     judge_offsets: tuple = ()  # per-digit gain offsets (tools/calibrate_judge.py)
+    # tensor parallelism (tp_spec): this rank's shard of a model split `tp_world` ways
+    tp_world: int = 1
+    tp_rank: int = 0
+    embed_rows: int = 0      # embedding rows when they differ from the LM-head shard (0: same)
+    vocab_base: int = 0      # global id of this rank's LM-head row 0
 
     @property
     def q_dim(self) -> int:
@@ -128,6 +133,65 @@ PAIRS = {
 }
 
 
+def tp_spec(spec: ModelSpec, rank: int, world: int) -> ModelSpec:
+    """Rank `rank`'s shard of `spec` under Megatron-style tensor parallelism
+    (SURVEY §8e): q/k/v heads and gate/up units column-parallel, O and down
+    row-parallel (their partial outputs all-reduced), LM head vocab-parallel,
+    embedding and norms replicated."""
+    if world == 1:
+        return spec
+    if spec.n_heads % world or spec.n_kv_heads % world:
+        raise ValueError(f"{spec.name}: heads {spec.n_heads}/{spec.n_kv_heads} not divisible by {world}")
+    if spec.d_ffn % (GU_BLOCK * world):
+        raise ValueError(f"{spec.name}: d_ffn {spec.d_ffn} not divisible by {GU_BLOCK * world}")
+    if spec.vocab_rows % (32 * world):
+        raise ValueError(f"{spec.name}: vocab rows {spec.vocab_rows} not divisible by {32 * world}")
+    vr = spec.vocab_rows // world
+    base = rank * vr
+    return replace(spec, name=f"{spec.name}-tp{rank}of{world}", n_heads=spec.n_heads // world,
+                   n_kv_heads=spec.n_kv_heads // world, d_ffn=spec.d_ffn // world,
+                   vocab_rows=vr, vocab_text=max(0, min(vr, spec.vocab_text - base)),
+                   embed_rows=spec.vocab_rows, vocab_base=base, tp_world=world, tp_rank=rank)
+
+
+def shard_tensor(name: str, t: torch.Tensor, spec: ModelSpec, rank: int, world: int) -> torch.Tensor:
+    """Rank `rank`'s slice of the full parameter `name` (see tp_spec)."""
+    if world == 1:
+        return t
+    leaf = name.rsplit(".", 1)[-1]
+    H, KV, f, hd = spec.n_heads // world, spec.n_kv_heads // world, spec.d_ffn // world, spec.head_dim
+    qd, kd = spec.q_dim, spec.kv_dim
+    q_rows = slice(rank * H * hd, (rank + 1) * H * hd)
+    if leaf in ("wqkv", "bqkv"):
+        k_rows = slice(qd + rank * KV * hd, qd + (rank + 1) * KV * hd)
+        v_rows = slice(qd + kd + rank * KV * hd, qd + kd + (rank + 1) * KV * hd)
+        return torch.cat([t[q_rows], t[k_rows], t[v_rows]]).contiguous()
+    if leaf == "wo":
+        return t[:, q_rows].contiguous()
+    if leaf == "wgu":                                     # whole 32-row gate/up blocks
+        return t[2 * rank * f:2 * (rank + 1) * f].contiguous()
+    if leaf == "wd":
+        return t[:, rank * f:(rank + 1) * f].contiguous()
+    if leaf == "lm_head":
+        vr = spec.vocab_rows // world
+        return t[rank * vr:(rank + 1) * vr].contiguous()
+    return t                                              # embed, norms: replicated
+
+
+def shard_weights(full: dict[str, torch.Tensor], spec: ModelSpec, rank: int,
+                  world: int) -> dict[str, torch.Tensor]:
+    """Slice a full model's weights into rank `rank`'s shard (see tp_spec)."""
+    return {k: shard_tensor(k, v, spec, rank, world) for k, v in full.items()}
+
+
+def make_tp_weights(spec: ModelSpec, rank: int, world: int, seed: int = 0,
+                    device: str = "cpu") -> dict[str, torch.Tensor]:
+    """Rank `rank`'s shard, generated tensor by tensor (peak memory: one full
+    tensor), identical to slicing make_weights(spec)."""
+    return {name: shard_tensor(name, make_tensor(spec, seed, name, device), spec, rank, world)
+            for name in tensor_shapes(spec)}
+
+
 def get_spec(name: str, **overrides) -> ModelSpec:
     spec = MODELS[name]
     return replace(spec, **overrides) if overrides else spec
@@ -145,7 +209,7 @@ def tensor_shapes(spec: ModelSpec) -> dict[str, tuple[int, ...]]:
     fused gate/up kernels consume.
     """
     d = spec.d_model
-    shapes: dict[str, tuple[int, ...]] = {"embed": (spec.vocab_rows, d), "ln_f": (d,),
+    shapes: dict[str, tuple[int, ...]] = {"embed": (spec.embed_rows or spec.vocab_rows, d), "ln_f": (d,),
                                           "lm_head": (spec.vocab_rows, d)}
     for i in range(spec.n_layers):
         p = f"layers.{i}."
