@@ -14,6 +14,7 @@
 // warps drain TMEM with tcgen05.ld.32x32b (warp w owns TMEM lanes 32w..32w+31
 // = weight rows) and write fp32 split partials, 128 B coalesced per token.
 #include <cuda.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -250,10 +251,13 @@ int make_tmap_bf16(void* out_map, const void* ptr, int rows, int cols, int box_r
 }
 
 int tc_token_tile(int M) {
-  if (M <= 32) return 32;
-  if (M <= 64) return 64;
-  if (M <= 128) return 128;
-  return 256;
+  static const int cap = [] {
+    const char* e = getenv("SR_GEMM_NT_MAX");  // tuning knob: largest token tile
+    const int v = e ? atoi(e) : 256;
+    return v == 32 || v == 64 || v == 128 ? v : 256;
+  }();
+  int t = M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+  return t < cap ? t : cap;
 }
 
 int tc_pick_splits(int M, int N, int K, int num_sms) {
@@ -270,8 +274,16 @@ int tc_pick_splits(int M, int N, int K, int num_sms) {
 template <int NT>
 static cudaError_t launch_nt(const TcGemmArgs& a, cudaStream_t stream) {
   constexpr int stage_bytes = kWStageBytes + NT * kBK * 2;
+  static const int max_stages = [] {
+    const char* e = getenv("SR_GEMM_STAGES");  // tuning knob (smaller: 2 CTAs per SM)
+    const int v = e ? atoi(e) : 8;
+    return v < 2 ? 2 : v > 8 ? 8 : v;
+  }();
   int stages = (200 * 1024) / stage_bytes;
-  if (stages > 8) stages = 8;
+  if (stages > max_stages) stages = max_stages;
+  // verify-sized token tiles: a 3-deep ring fits two CTAs per SM, so one
+  // CTA's TMEM drain overlaps the other's main loop (measured ~4 % at M = 80)
+  if (NT <= 128 && max_stages == 8) stages = 3;
   const int smem = stages * stage_bytes + 1024;
   static bool attr = false;
   if (!attr) {

@@ -70,7 +70,9 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
   L.q = take(T * qd * 2);
   L.attn = take(T * qd * 2);
   L.act = take(T * d.d_ffn * 2);
-  L.part_floats = (size_t)kPrefillSplitsMax * T * nmax;
+  // split-K partials: up to 8 splits for short (verify-sized) chunks; long
+  // chunks have enough output tiles for one split (gemm() lowers the count)
+  L.part_floats = (size_t)std::max<size_t>((size_t)kPrefillSplitsMax * std::min<size_t>(T, 256), T) * nmax;
   L.part = take(L.part_floats * 4);
   L.apart = take(T * d.n_heads * nsplit_max * (SR_HEAD_DIM + 2) * 4);
   L.actr = take(T * d.n_kv_heads * 4);

@@ -24,13 +24,14 @@ def main() -> None:
     ap.add_argument("--ctx", type=int, default=2048)
     ap.add_argument("--m", type=int, default=80)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--max-tokens", type=int, default=256, help="largest prefill chunk")
     a = ap.parse_args()
     from paper_2504_07891_b200.backend import B200Backend
     from paper_2504_07891_b200.domain import BackendRole
     from paper_2504_07891_b200.shapes import get_spec
 
     spec = get_spec(a.model)
-    b = B200Backend(spec, BackendRole.BASE, max_ctx=a.ctx + a.m + 64)
+    b = B200Backend(spec, BackendRole.BASE, max_ctx=a.ctx + a.m + 64, max_tokens=a.max_tokens)
     eng = b.engine
     g = torch.Generator().manual_seed(0)
     ctx = torch.randint(16, spec.vocab_text, (a.ctx,), generator=g).tolist()
