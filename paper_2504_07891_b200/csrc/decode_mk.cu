@@ -145,16 +145,15 @@ SR_DEV float mk_sum_parts(const float* part, const uint16_t* tab, int row, int m
   const int c0 = e & 0xff, n = (e >> 8) & 0xf, j0 = e >> 12;
   const size_t cs = (size_t)maxj * kTR;
   const float* q1 = part + (size_t)(c0 + 1) * cs + r;
-  // up to four contributors as independent predicated loads (all in flight
-  // together); more only for tiny models
-  const float a0 = __ldcg(part + (size_t)c0 * cs + (size_t)j0 * kTR + r);
-  const float a1 = n > 1 ? __ldcg(q1) : 0.f;
-  const float a2 = n > 2 ? __ldcg(q1 + cs) : 0.f;
-  const float a3 = n > 3 ? __ldcg(q1 + 2 * cs) : 0.f;
-  float s = ((a0 + a1) + a2) + a3;
-  if (n > 4) {
-    for (int q = 4; q < n; ++q) s += __ldcg(part + (size_t)(c0 + q) * cs + r);
-  }
+  // up to eight contributors as independent predicated loads, all in flight
+  // together (no loop: the unrolled callers keep every row's loads batched)
+  float a[8];
+  a[0] = __ldcg(part + (size_t)c0 * cs + (size_t)j0 * kTR + r);
+#pragma unroll
+  for (int q = 1; q < 8; ++q) a[q] = n > q ? __ldcg(q1 + (size_t)(q - 1) * cs) : 0.f;
+  float s = a[0];
+#pragma unroll
+  for (int q = 1; q < 8; ++q) s += a[q];
   return s;
 }
 
@@ -318,6 +317,7 @@ SR_DEV void mk_gemv(const MkParams& p, const PhaseInfo& pi, int c, const uint8_t
     }
   }
 }
+
 
 SR_DEV float mk_qkv_val(const MkParams& p, const __nv_bfloat16* bias, const uint16_t* tab,
                         int row) {
@@ -813,8 +813,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, npages, scratch, kvbuf,
                    &kvbar, kvpar);
       if (p.prof && threadIdx.x == 0 && l == 1 && tstep < 40) {  // per-CTA attention time, layer 1
-        p.prof[1024 + c] = global_ns() - ta0;
-        p.prof[1024 + 256 + c] = (c % S_a) == S_a - 1;
+        p.prof[1280 + c] = global_ns() - ta0;
+        p.prof[1440 + c] = (c % S_a) == S_a - 1;
       }
       // warm L2 with what the next layer reads on its latency-bound path
       if (threadIdx.x == 0) mk_prefetch_next_layer(p, l + 1, pos, page_table, c, G, S_a, npages);

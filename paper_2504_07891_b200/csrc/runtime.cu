@@ -197,7 +197,7 @@ struct Model {
           auto first = [&](long c) { return T >= G ? T * c / G : std::min(c, T); };
           const long c0 = owner(u0), c1 = owner(u1);
           const long j0 = b - first(c0) / kt;
-          if (j0 >= L.mk_maxj || j0 > 15 || c1 - c0 + 1 > 15)
+          if (j0 >= L.mk_maxj || j0 > 15 || c1 - c0 + 1 > 8)
             return fail(SR_E_INVALID, "decode partial tables out of range");
           tab[t * 256 + b] = (uint16_t)(c0 | (c1 - c0 + 1) << 8 | j0 << 12);
         }

@@ -65,8 +65,8 @@ def main() -> None:
                     "select": round((tail[3] - tail[2]) / 1e3, 2)}
     out["token_us"] = round((t[n - 1] - t[0]) / 1e3, 1)
     import statistics
-    att = ev[1024:1024 + 148]
-    last = ev[1280:1280 + 148]
+    att = ev[1280:1280 + 148]
+    last = ev[1440:1440 + 148]
     busy = [x / 1e3 for x in att if x > 0]
     if busy:
         out["attn_cta_us"] = {"n": len(busy), "min": round(min(busy), 2),
