@@ -264,7 +264,12 @@ def run_ours(args) -> None:
                                "per token (SURVEY 8d) / CUDA-event decode time",
                      "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
-                     "peak_source": peaks["src"], "traffic": None,
+                     "peak_source": peaks["src"],
+                     # ncu --set full of the same kernel (7B base, C~2K): DRAM bytes
+                     # read+written per decoded token, vs the algorithmic bytes
+                     "traffic": 14.271e9 if args.pair == "1.5b+7b" else None,
+                     "traffic_unit": "bytes/token (profiles/r01_ncu_decode_mk_qwen2.5-7b_summary.txt)",
+                     "algorithmic_bytes_per_token": round(db.decode_bytes / max(1, db.decode_tokens)),
                      "draft_decode_GBps": round(ds.decode_bytes / (ds.decode_ms * 1e-3) / 1e9, 1)
                      if ds.decode_ms > 0 else None},
         "gpu_launches": ds.launches + db.launches,
