@@ -182,6 +182,8 @@ def run_ours(args) -> None:
         base_tp = TensorParallel.from_dist() if dist is not None else TensorParallel.single()
     small, base = build_pair(args.pair, seed=args.seed, max_ctx=args.budget + 512,
                              threshold=args.threshold, base_tp=base_tp)
+    if args.spec_gamma > 0:  # SpecReason+Decode: the draft proposes tokens inside base fallback
+        base.attach_speculator(small, gamma=args.spec_gamma)
     vocab = shared_vocab(get_spec(PAIRS[args.pair][0]).vocab_text)
     cfg = EngineConfig(threshold=AcceptanceThreshold(args.threshold), temperature=0.0,
                        token_budget=args.budget, max_step_tokens=args.max_step_tokens)
@@ -451,6 +453,8 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--spec-gamma", type=int, default=0,
+                    help="token-level speculation inside base generation (0 = off)")
     ap.add_argument("--mode", default="dp", choices=["dp", "tp"],
                     help="multi-GPU: dp = independent problems per rank (C5), "
                          "tp = base model tensor-parallel over the ranks (C4)")

@@ -160,6 +160,17 @@ int sr_score(void* model, const int32_t* page_table, int32_t start_pos,
              int32_t threshold, sr_readout* readout, void* stream);
 
 /*
+ * Token-level speculation (SpecReason+Decode): prefill ids at start_pos..
+ * (n_ids <= max_tokens) and write the greedy choice after every fed token:
+ * out_ids[i] = argmax of the logits at position start_pos + i (ties: lower
+ * id), margins[i] (may be NULL) = top-1 minus top-2.  The LM head runs as
+ * one tensor-core GEMM over all rows.
+ */
+int sr_verify_tokens(void* model, const int32_t* page_table, int32_t start_pos,
+                     const int32_t* ids, int32_t n_ids, int32_t* out_ids, float* margins,
+                     void* stream);
+
+/*
  * Test hook: prefill ids and write fp32 logits of every new position
  * (`all` != 0, logits [n_ids, vocab_rows]) or of the last one ([vocab_rows]).
  */

@@ -83,6 +83,16 @@ class RefEngine:
         stream.ids.extend(suffix)
         return judge_readout(logits, self.vocab, threshold)
 
+    def prefill(self, stream: Stream, suffix: Sequence[int]) -> None:
+        self.model.forward(stream.handle, list(suffix))
+        stream.ids.extend(suffix)
+
+    def verify_tokens(self, stream: Stream, suffix: Sequence[int]) -> tuple[list[int], list[float]]:
+        logits = self.model.forward(stream.handle, list(suffix), last_only=False)
+        stream.ids.extend(suffix)
+        out = [argmax_margin(masked(row, self.vocab.n_text)) for row in logits]
+        return [t for t, _ in out], [m for _, m in out]
+
     def logits_teacher_forced(self, ids: Sequence[int]) -> torch.Tensor:
         """[n, V] logits of every position of ``ids`` from an empty cache."""
         cache = self.model.new_cache()

@@ -292,6 +292,28 @@ class NativeEngine:
         return Readout(score=int(r[0]), accept=bool(int(r[1])), flags=0, margin=margin,
                        argmax=int(r[3]))
 
+    def prefill(self, stream: Stream, suffix: Sequence[int]) -> None:
+        """Commit ``suffix`` to the stream's K/V (no token is chosen)."""
+        self.forward_logits(stream, suffix, all_rows=False)
+
+    def verify_tokens(self, stream: Stream, suffix: Sequence[int]) -> tuple[list[int], list[float]]:
+        """Prefill ``suffix`` and return the greedy choice after every fed
+        token (token-level speculation, ``sr_verify_tokens``)."""
+        m = self.model
+        start = len(stream.ids)
+        n = len(suffix)
+        self._ensure(stream, start + n)
+        ids_ptr = m.upload_ids(suffix)
+        native.check("sr_verify_tokens", m.lib.sr_verify_tokens(
+            m.handle, C.c_void_p(stream.handle.table_dev.data_ptr()), start, C.c_void_p(ids_ptr), n,
+            C.c_void_p(m.out_dev.data_ptr()), C.c_void_p(m.margin_dev.data_ptr()), m.stream_ptr))
+        m.out_host[:n].copy_(m.out_dev[:n], non_blocking=True)
+        m.margin_host[:n].copy_(m.margin_dev[:n], non_blocking=True)
+        torch.cuda.current_stream(m.device).synchronize()
+        self.stats.add_score(m, n, start)
+        stream.ids.extend(suffix)
+        return m.out_host[:n].tolist(), m.margin_host[:n].tolist()
+
     def forward_logits(self, stream: Stream, suffix: Sequence[int], all_rows: bool = True) -> torch.Tensor:
         """Test hook: prefill ``suffix`` and return fp32 logits (device)."""
         m = self.model

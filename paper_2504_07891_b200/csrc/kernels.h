@@ -159,6 +159,11 @@ cudaError_t epi_qkv_launch(const EpiParams& p, cudaStream_t stream);
 cudaError_t epi_resid_norm_launch(const EpiParams& p, cudaStream_t stream);
 cudaError_t epi_glu_launch(const EpiParams& p, cudaStream_t stream);
 
+// per-row greedy choice over split LM-head partials (token-level speculation)
+cudaError_t rows_argmax_launch(const float* part, int splits, size_t stride, int rows, int N,
+                               int n_valid, int base, int32_t* out_ids, float* margins,
+                               cudaStream_t stream);
+
 // verify readout over fp32 logits [V]
 struct ReadoutParams {
   const float* logits;

@@ -296,6 +296,43 @@ cudaError_t epi_glu_launch(const EpiParams& p, cudaStream_t stream) {
   return launch_pdl(epi_glu_kernel, grid, kEpiThreads, 0, stream, p);
 }
 
+// ================================================ per-row greedy choices ====
+// rows x vocab logits (sum of split partials) -> argmax (ties: lower id) and
+// top-1 minus top-2 margin per row; one CTA per row
+__global__ void __launch_bounds__(1024) rows_argmax_kernel(const float* part, int splits,
+                                                           size_t stride, int N, int n_valid,
+                                                           int base, int32_t* out_ids,
+                                                           float* margins) {
+  grid_wait();
+  __shared__ float s1[32], s2[32];
+  __shared__ int si[32];
+  const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Top2 b;
+  b.init();
+  for (int v = tid; v < n_valid; v += blockDim.x) {
+    float x = 0.f;
+    for (int sp = 0; sp < splits; ++sp) x += __ldcg(part + sp * stride + (size_t)r * N + v);
+    b.push(x, base + v);
+  }
+  warp_top2(b);
+  if (lane == 0) { s1[warp] = b.v1; s2[warp] = b.v2; si[warp] = b.i1; }
+  __syncthreads();
+  if (tid == 0) {
+    Top2 f;
+    f.init();
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) f.merge(s1[w], si[w], s2[w]);
+    out_ids[r] = f.i1;
+    if (margins) margins[r] = f.v1 - f.v2;
+  }
+}
+
+cudaError_t rows_argmax_launch(const float* part, int splits, size_t stride, int rows, int N,
+                               int n_valid, int base, int32_t* out_ids, float* margins,
+                               cudaStream_t stream) {
+  return launch_pdl(rows_argmax_kernel, dim3(rows), 1024, 0, stream, part, splits, stride, N,
+                    n_valid, base, out_ids, margins);
+}
+
 // ======================================================= verify readout ====
 // Pass 1 (grid-wide): greedy top-2 partials and, for each digit d, the count
 // of valid ids ranked before it (logit greater, or equal with a lower id).

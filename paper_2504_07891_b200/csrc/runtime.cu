@@ -958,6 +958,35 @@ int sr_forward_logits(void* model, const int32_t* page_table, int32_t start_pos,
   return 0;
 }
 
+int sr_verify_tokens(void* model, const int32_t* page_table, int32_t start_pos,
+                     const int32_t* ids, int32_t n_ids, int32_t* out_ids, float* margins,
+                     void* stream) {
+  Model* m = (Model*)model;
+  if (!m || !page_table || !ids || !out_ids) return fail(SR_E_INVALID, "null argument");
+  if (n_ids < 1 || start_pos < 0 || start_pos + n_ids > m->d.max_pos)
+    return fail(SR_E_INVALID, "bad sizes");
+  if (n_ids > m->d.max_tokens) return fail(SR_E_CAPACITY, "n_ids exceeds max_tokens");
+  if (m->tp_comm) return fail(SR_E_INVALID, "sr_verify_tokens: tensor parallelism not supported");
+  cudaStream_t s = (cudaStream_t)stream;
+  SR_CK(cudaEventRecord(m->ev[0], s));
+  int rows = 0;
+  int rc = m->prefill(page_table, start_pos, ids, n_ids, s, &rows);
+  if (rc) return -rc;
+  // LM head for every row as one tcgen05 GEMM, then a per-row argmax
+  const size_t need = (size_t)rows * m->d.vocab_rows;
+  if (need > m->L.part_floats) return fail(SR_E_CAPACITY, "LM-head partials exceed the workspace");
+  rc = m->gemm(Model::ACT_X, m->d.n_layers * 4, m->x, m->lm_head, rows, m->d.vocab_rows,
+               m->d.d_model, s);
+  if (rc) return -rc;
+  SR_CK(rows_argmax_launch(m->part, m->last_splits, need, rows, m->d.vocab_rows, m->d.vocab_text,
+                           m->d.vocab_base, out_ids, margins, s));
+  SR_CK(cudaEventRecord(m->ev[1], s));
+  SR_CK(cudaEventRecord(m->ev[2], s));
+  m->timing.prefill_tokens = n_ids;
+  m->timing.decode_tokens = 0;
+  return 0;
+}
+
 int sr_tp_unique_id(uint8_t* h_id128) {
   if (!h_id128) return fail(SR_E_INVALID, "null argument");
   if (!tp_available()) return fail(SR_E_TP, "libnccl.so.2 not loadable");

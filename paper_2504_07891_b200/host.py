@@ -42,7 +42,7 @@ from typing import Any, Protocol, Sequence
 from . import contract, domain
 from .contract import Backend, GenerationRequest, VerificationRequest
 from .domain import BackendProfile
-from .vocab import CLASS_END_THINK, CLASS_STOP, Vocab
+from .vocab import CLASS_END_THINK, CLASS_MASKED, CLASS_STOP, Vocab
 
 # finish codes shared with the device (include/specreason_b200.h)
 FINISH_LENGTH = 0
@@ -202,6 +202,65 @@ class ModelBackend(Backend):
         self.record = record
         self.calls: list[dict] = []   # per-call trace (ids) for replay parity
 
+    # -- token-level speculation (SpecReason+Decode) ----------
+    def attach_speculator(self, draft: "ModelBackend", gamma: int = 5) -> None:
+        """Decode this (base) backend's steps with `draft` proposing `gamma`
+        tokens per round and one verify pass accepting the longest prefix the
+        greedy base agrees with, plus the base's own next token (lossless for
+        greedy decoding: ``speculative_decode``, specdecode.py:120-177)."""
+        if draft.vocab.n_text != self.vocab.n_text:
+            raise ValueError("speculator must share the vocabulary")
+        self.speculator = draft
+        self.spec_gamma = int(gamma)
+        self.spec_stats = {"rounds": 0, "proposed": 0, "accepted": 0}
+
+    def _generate_speculative(self, ids: list[int], max_tokens: int,
+                              stop: tuple[str, ...]) -> tuple[list[int], int]:
+        d = self.speculator
+        classes = self.vocab.token_classes(stop, max(self.vocab.n_text, 16))
+        stream, keep = self.pool.acquire(ids)
+        self.engine.truncate(stream, keep)
+        ctx = list(ids)
+        out: list[int] = []
+        finish = FINISH_LENGTH
+        with d._lock:
+            dstream, dkeep = d.pool.acquire(ids)
+            d.engine.truncate(dstream, dkeep)
+            while True:
+                budget = max_tokens - len(out)
+                gamma = min(self.spec_gamma, budget)
+                drafts: list[int] = []
+                if gamma > 1:  # the verify pass always adds one base token itself
+                    drafts, _ = d.engine.generate(dstream, ctx[len(dstream.ids):], gamma - 1, stop)
+                if len(stream.ids) < len(ctx) - 1:  # catch the base stream up first
+                    self.engine.prefill(stream, ctx[len(stream.ids):-1])
+                choices, _ = self.engine.verify_tokens(stream, [ctx[-1]] + drafts)
+                k = 0
+                while k < len(drafts) and choices[k] == drafts[k]:
+                    k += 1
+                new = drafts[:k] + [choices[k]]
+                self.spec_stats["rounds"] += 1
+                self.spec_stats["proposed"] += len(drafts)
+                self.spec_stats["accepted"] += k
+                done = False
+                for t in new:
+                    out.append(t)
+                    ctx.append(t)
+                    c = int(classes[t]) if t < len(classes) else CLASS_MASKED
+                    if c == CLASS_END_THINK:
+                        finish, done = FINISH_END_THINK, True
+                    elif c == CLASS_STOP:
+                        finish, done = FINISH_STOP, True
+                    elif len(out) >= max_tokens:
+                        done = True
+                    if done:
+                        break
+                # roll both streams back to the committed context (KV of ctx[:-1])
+                self.engine.truncate(stream, min(len(stream.ids), len(ctx) - 1))
+                d.engine.truncate(dstream, min(common_prefix(dstream.ids, ctx), len(ctx) - 1))
+                if done:
+                    return out, finish
+
     # -- API -------------------------------------------------------------
     def generate_step(self, request: GenerationRequest):
         if not request.prompt:
@@ -209,10 +268,15 @@ class ModelBackend(Backend):
         t0 = time.monotonic()
         with self._lock:
             ids = self._prompts.encode(request.prompt)
-            stream, keep = self.pool.acquire(ids)
-            self.engine.truncate(stream, keep)
-            gen, finish = self.engine.generate(stream, ids[keep:], request.max_tokens,
-                                               tuple(request.stop))
+            if getattr(self, "speculator", None) is not None:
+                gen, finish = self._generate_speculative(ids, request.max_tokens,
+                                                         tuple(request.stop))
+                keep = len(ids)
+            else:
+                stream, keep = self.pool.acquire(ids)
+                self.engine.truncate(stream, keep)
+                gen, finish = self.engine.generate(stream, ids[keep:], request.max_tokens,
+                                                   tuple(request.stop))
             if self.record:
                 self.calls.append({"kind": "gen", "prompt_ids": ids, "gen_ids": list(gen),
                                    "finish": finish, "stop": list(request.stop),
