@@ -111,13 +111,15 @@ def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        local = local % torch.cuda.device_count()  # more ranks than GPUs: share (testing)
     if world > 1:
         import torch.distributed as dist
 
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
-            torch.cuda.set_device(local)
-        dist.init_process_group(backend, rank=rank, world_size=world)
+        # the data path has no torch collective: DP ranks are independent and
+        # TP uses the library's own NCCL communicator (only its 128-byte id
+        # travels through torch.distributed), so gloo carries the few scalars
+        dist.init_process_group("gloo", rank=rank, world_size=world)
         return dist, rank, world, local
     return None, 0, 1, local
 
@@ -125,7 +127,7 @@ def _dist():
 def _reduce_max(dist, v: float) -> float:
     if dist is None:
         return v
-    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    t = torch.tensor([v], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -133,7 +135,7 @@ def _reduce_max(dist, v: float) -> float:
 def _reduce_sum(dist, v: float) -> float:
     if dist is None:
         return v
-    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    t = torch.tensor([v], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
