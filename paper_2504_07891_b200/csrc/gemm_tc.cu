@@ -68,7 +68,8 @@ SR_DEV void umma_commit(uint64_t* bar) {
 template <int NT>
 __global__ void __launch_bounds__(kTcThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                   float* __restrict__ C, int M, int N, int nkb_total, int splits, int stages) {
+                   float* __restrict__ C, int M, int N, int nkb_total, int splits, int stages,
+                   __nv_bfloat16* __restrict__ act) {
   extern __shared__ uint8_t smem_dyn[];
   __shared__ __align__(8) uint64_t full_bar[8];
   __shared__ __align__(8) uint64_t empty_bar[8];
@@ -184,7 +185,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             "=r"(v[31])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < N) {
+      if (act != nullptr) {
+        // gate/up fused epilogue: warp w holds one 32-row block of the
+        // interleaved layout -- lanes 0-15 gate units, lanes 16-31 their up
+        const int f = N >> 1;
+        const int unit = ((n0 + warp * 32) >> 5) * 16 + (lane & 15);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float g = __uint_as_float(v[c]);
+          const float u = __shfl_down_sync(0xffffffffu, g, 16);
+          const int m = m0 + j + c;
+          if (lane < 16 && m < M && row < N)
+            act[(size_t)m * f + unit] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
+        }
+      } else if (row < N) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const int m = m0 + j + c;
@@ -303,7 +317,8 @@ static cudaError_t launch_nt(const TcGemmArgs& a, cudaStream_t stream) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<NT>, *(const CUtensorMap*)a.tmW,
-                            *(const CUtensorMap*)a.tmX, a.C, a.M, a.N, a.K / kBK, a.splits, stages);
+                            *(const CUtensorMap*)a.tmX, a.C, a.M, a.N, a.K / kBK, a.splits, stages,
+                            a.splits == 1 ? a.act : nullptr);
 }
 
 cudaError_t gemm_tc_launch(const TcGemmArgs& a, cudaStream_t stream) {

@@ -124,6 +124,8 @@ struct TcGemmArgs {
   const void* tmX;  // X [M_cap, K], box 64 x tc_token_tile(M)
   float* C;         // [splits, M, N]
   int M, N, K, splits;
+  __nv_bfloat16* act;  // non-null (splits == 1, interleaved gate/up W): write
+                       // bf16 silu(gate) * up [M, N/2] instead of C
 };
 int make_tmap_bf16(void* out_map, const void* ptr, int rows, int cols, int box_rows);
 int make_tmap_bf16_box(void* out_map, const void* ptr, int rows, int cols, int box_cols,

@@ -462,10 +462,12 @@ struct Model {
           if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
         SR_CK(epi_resid_norm_launch(ep, s));
         // gate/up
-        rc = gemm(ACT_X, l * 4 + 2, x, lw(l, WGU), M, 2 * d.d_ffn, d.d_model, s);
+        rc = gemm(ACT_X, l * 4 + 2, x, lw(l, WGU), M, 2 * d.d_ffn, d.d_model, s, act);
         if (rc) return -rc;
-        ep = epi_base(M, 2 * d.d_ffn);
-        SR_CK(epi_glu_launch(ep, s));
+        if (!fused_glu) {
+          ep = epi_base(M, 2 * d.d_ffn);
+          SR_CK(epi_glu_launch(ep, s));
+        }
         watch(s, "o/gu gemm+epi", l, M, last_splits);
         // down + residual + next norm
         rc = gemm(ACT_ACT, l * 4 + 3, act, lw(l, WD), M, d.d_model, d.d_ffn, s);
@@ -574,6 +576,7 @@ struct Model {
   }
 
   int last_splits = 1;
+  bool fused_glu = false;  // the last gemm() wrote silu(gate)*up itself
   // SR_WATCH=1: synchronise after each prefill stage and abort with the stage
   // name if it does not finish within 10 s (bring-up aid for device hangs)
   bool watch_on = false;
@@ -596,9 +599,11 @@ struct Model {
   }
 
   int gemm(int act_id, int wmap, const __nv_bfloat16* A, const __nv_bfloat16* B, int M, int N,
-           int K, cudaStream_t s) {
+           int K, cudaStream_t s, __nv_bfloat16* glu_out = nullptr) {
+    fused_glu = false;
     if (use_tc) {
       TcGemmArgs a{};
+      a.act = glu_out;
       const int nt = tc_token_tile(M);
       const int ti = nt == 32 ? 0 : nt == 64 ? 1 : nt == 128 ? 2 : 3;
       a.tmW = &wmaps[wmap].m;
@@ -611,6 +616,7 @@ struct Model {
       while (sp > 1 && (size_t)sp * M * N > L.part_floats) --sp;
       a.splits = sp;
       last_splits = sp;
+      fused_glu = glu_out != nullptr && sp == 1;
       SR_CK(gemm_tc_launch(a, s));
       return 0;
     }

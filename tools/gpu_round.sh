@@ -1,4 +1,4 @@
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 6 --warmup 3 > gpurun_out/bench_dp2.log 2>&1
-tail -2 gpurun_out/bench_dp2.log | cut -c1-700
-timeout 1500 python bench.py --pair 1.5b+32b --budget 8192 --steps 12 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.log 2>&1
-tail -1 gpurun_out/bench_c3.log | cut -c1-1600
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullwidth.py -x -q 2>&1 | tail -2
+timeout 300 python tools/verify_profile.py qwen2.5-7b --ctx 2048 --m 80 2>&1 | tail -1 | cut -c1-150
+timeout 300 python tools/verify_profile.py r1-1.5b --ctx 2048 --m 80 2>&1 | tail -1 | cut -c1-150
+timeout 300 python tools/verify_profile.py qwen2.5-7b --ctx 2048 --m 640 --max-tokens 1024 --reps 3 2>&1 | tail -1 | cut -c1-150
