@@ -278,7 +278,13 @@ int tc_pick_splits(int M, int N, int K, int num_sms) {
   const int nt = tc_token_tile(M);
   const int tiles = ((N + kWRows - 1) / kWRows) * ((M + nt - 1) / nt);
   const int nkb = K / kBK;
-  int s = num_sms / tiles;
+  // token tiles <= 128 run a 3-stage ring, two CTAs per SM: fill both slots
+  static const int per_sm = [] {
+    const char* e = getenv("SR_GEMM_CTAS_PER_SM");
+    const int v = e ? atoi(e) : 2;
+    return v < 1 ? 1 : v > 2 ? 2 : v;
+  }();
+  int s = (nt <= 128 ? per_sm : 1) * num_sms / tiles;
   if (s < 1) s = 1;
   if (s > 8) s = 8;
   while (s > 1 && nkb / s < 4) --s;
