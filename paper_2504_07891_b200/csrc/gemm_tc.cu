@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   constexpr int kXStageBytes = NT * kBK * 2;
   constexpr int kStageBytes = kWStageBytes + kXStageBytes;
-  constexpr int kTmemCols = NT < 32 ? 32 : NT;
+  // TMEM columns are allocated in powers of two >= 32
+  constexpr int kTmemCols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kWRows, m0 = blockIdx.y * NT, split = blockIdx.z;
@@ -268,9 +269,11 @@ int tc_token_tile(int M) {
   static const int cap = [] {
     const char* e = getenv("SR_GEMM_NT_MAX");  // tuning knob: largest token tile
     const int v = e ? atoi(e) : 256;
-    return v == 32 || v == 64 || v == 128 ? v : 256;
+    return v == 32 || v == 64 || v == 96 || v == 128 ? v : 256;
   }();
-  int t = M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+  // 96: verify passes (~60-100 tokens) would waste a third of a 128 tile's
+  // activation traffic and MMA work
+  int t = M <= 32 ? 32 : M <= 64 ? 64 : M <= 96 ? 96 : M <= 128 ? 128 : 256;
   return t < cap ? t : cap;
 }
 
@@ -332,6 +335,7 @@ cudaError_t gemm_tc_launch(const TcGemmArgs& a, cudaStream_t stream) {
   switch (tc_token_tile(a.M)) {
     case 32: return launch_nt<32>(a, stream);
     case 64: return launch_nt<64>(a, stream);
+    case 96: return launch_nt<96>(a, stream);
     case 128: return launch_nt<128>(a, stream);
     default: return launch_nt<256>(a, stream);
   }

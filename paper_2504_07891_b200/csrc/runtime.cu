@@ -137,7 +137,7 @@ struct Model {
   bool prefetch = false;       // SR_PREFETCH=1: GEMV L2 prefetch before the PDL wait
   struct alignas(64) TMap { CUtensorMap m; };
   std::vector<TMap> wmaps;     // per layer: qkv, o, gu, d ; then lm_head
-  TMap amaps[3][4];            // [x | attn | act][token tile 32/64/128/256]
+  TMap amaps[3][5];            // [x | attn | act][token tile 32/64/96/128/256]
   enum { ACT_X = 0, ACT_ATTN = 1, ACT_ACT = 2 };
 
   int build_tmaps() {
@@ -154,9 +154,9 @@ struct Model {
       return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for lm_head");
     const void* a[3] = {x, attn, act};
     const int acols[3] = {d.d_model, q_dim, d.d_ffn};
-    const int tiles[4] = {32, 64, 128, 256};
+    const int tiles[5] = {32, 64, 96, 128, 256};
     for (int i = 0; i < 3; ++i)
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < 5; ++t)
         if (make_tmap_bf16(&amaps[i][t].m, a[i], d.max_tokens, acols[i], tiles[t]))
           return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for an activation");
     return 0;
@@ -605,7 +605,7 @@ struct Model {
       TcGemmArgs a{};
       a.act = glu_out;
       const int nt = tc_token_tile(M);
-      const int ti = nt == 32 ? 0 : nt == 64 ? 1 : nt == 128 ? 2 : 3;
+      const int ti = nt == 32 ? 0 : nt == 64 ? 1 : nt == 96 ? 2 : nt == 128 ? 3 : 4;
       a.tmW = &wmaps[wmap].m;
       a.tmX = &amaps[act_id][ti].m;
       a.C = part;
