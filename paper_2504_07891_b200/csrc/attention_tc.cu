@@ -75,7 +75,7 @@ struct Flash {
   float m[2], l[2];
 };
 
-template <bool CAUSAL>
+template <bool CAUSAL, bool PLO = true>
 SR_DEV void flash_tile(Flash& F, const uint32_t (&qa)[8][4], uint32_t ks, uint32_t vs, int lane,
                        int tile_pos0, int lim0, int lim1) {
   // S = Q K^T for 16 rows x 64 positions
@@ -161,8 +161,10 @@ SR_DEV void flash_tile(Flash& F, const uint32_t (&qa)[8][4], uint32_t ks, uint32
       ldsm4t(b, vs + swz(row, chunk));
       mma_bf16(F.o[2 * dp], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b[0], b[1]);
       mma_bf16(F.o[2 * dp + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b[2], b[3]);
-      mma_bf16(F.o[2 * dp], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b[0], b[1]);
-      mma_bf16(F.o[2 * dp + 1], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b[2], b[3]);
+      if (PLO) {
+        mma_bf16(F.o[2 * dp], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b[0], b[1]);
+        mma_bf16(F.o[2 * dp + 1], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b[2], b[3]);
+      }
     }
   }
 }
@@ -263,8 +265,13 @@ __global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams
       const int warp_lim = start + (row0 + my_rows0) / G;
       const bool need_mask = pos0 + kTile - 1 > warp_lim;
       const uint32_t ks = s_u32(sm.k[buf]), vs = s_u32(sm.v[buf]);
-      if (need_mask) flash_tile<true>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
-      else flash_tile<false>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
+      if (p.p_hi_only) {  // P as plain bf16 (one P.V product)
+        if (need_mask) flash_tile<true, false>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
+        else flash_tile<false, false>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
+      } else {
+        if (need_mask) flash_tile<true>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
+        else flash_tile<false>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
+      }
     }
     __syncthreads();
   }

@@ -92,6 +92,7 @@ struct AttnParams {
   int layer, n_pages, n_heads, n_kv, nsplit;
   int start_pos;             // prefill: position of row 0
   int sep_merge;             // prefill: leave split partials for attn_merge_launch
+  int p_hi_only;             // prefill: P.V with bf16 P only (no hi/lo split)
   DecodeState* st;           // decode: ctx_len / page table from here
 };
 

@@ -449,6 +449,7 @@ struct Model {
           const int q_tiles = (M * G + 63) / 64;
           a.nsplit = std::min(kAttnPrefillSplit, attn_tc_splits(d.n_kv_heads, q_tiles, Tlast, num_sms));
           a.sep_merge = 1;
+          a.p_hi_only = p_hi_only ? 1 : 0;
           SR_CK(attn_tc_launch(a, M, a.nsplit, s, true));
           if (a.nsplit > 1) SR_CK(attn_merge_launch(a, M, a.nsplit, s));
           watch(s, "attn_prefill_tc", l, M, a.nsplit);
@@ -577,6 +578,10 @@ struct Model {
 
   int last_splits = 1;
   bool fused_glu = false;  // the last gemm() wrote silu(gate)*up itself
+  // SR_ATTN_PHI=1: prefill attention with bf16 P only.  Off: the hi/lo split
+  // of P is needed for the tiny-model parity bound (measured: bf16 P fails
+  // tests/test_gpu_parity.py) and costs only ~2-3 % of a verify pass
+  bool p_hi_only = false;
   // SR_WATCH=1: synchronise after each prefill stage and abort with the stage
   // name if it does not finish within 10 s (bring-up aid for device hangs)
   bool watch_on = false;
@@ -754,6 +759,7 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
   }
   if (const char* v = getenv("SR_ATTN")) m->attn_simt = strcmp(v, "simt") == 0;
   if (const char* v = getenv("SR_PREFETCH")) m->prefetch = v[0] == '1';
+  if (const char* v = getenv("SR_ATTN_PHI")) m->p_hi_only = v[0] == '1';
   if (const char* v = getenv("SR_WATCH")) {
     m->watch_on = atoi(v) > 0;
     m->watch_ms = atoi(v) > 1 ? atoi(v) * 1000 : 10000;
