@@ -55,8 +55,15 @@
 
 namespace sr {
 
-constexpr int kMkWarps = 16;
+#ifndef SR_MK_WARPS
+#define SR_MK_WARPS 16
+#endif
+constexpr int kMkWarps = SR_MK_WARPS;      // consumer warps (16 or 8)
 constexpr int kMkConsumers = kMkWarps * 32;
+constexpr int kRW = 32 / kMkWarps;          // rows of a 32-row tile per warp
+constexpr int kGroups = kMkConsumers / 128; // attention P.V position groups
+constexpr int kPPG = 64 / kGroups;          // positions per P.V group
+constexpr int kPosPass = 4 * kMkWarps;      // positions per score pass
 constexpr int kMkThreads = kMkConsumers + 32;
 constexpr int kTR = 32;                    // tile rows
 constexpr int kTC = 256;                   // tile columns (bf16)
@@ -71,7 +78,7 @@ constexpr int kMkMaxGq = 8;
 constexpr int kMkProfEvents = SR_PROF_EVENTS;
 constexpr int kMkNorm = 5120 / kMkConsumers;
 constexpr int kMkAttnScratchFloats =
-    kMkMaxGq * 128 + kMkMaxGq * 64 + 3 * kMkMaxGq + 4 * kMkMaxGq * 128 + 2 * 128;
+    kMkMaxGq * 128 + kMkMaxGq * 64 + 3 * kMkMaxGq + kGroups * kMkMaxGq * 128 + 2 * 128;
 constexpr int kMkTab = 256;
 constexpr int kKvBufBytes = 2 * kPage * kHeadDim * 2;  // 32 KB  // max 32-row blocks of a tile-range phase (smem tables)
 
@@ -197,38 +204,76 @@ SR_DEV void mk_grid_sync(unsigned* ctr, unsigned& target, int G, int sleep_ns) {
 }
 
 // x = bf16(h * rstd * w) with h = embedding row (mode 0) or hin + partials;
-// zero padding up to the next multiple of 256; CTA 0 stores h to hout
+// zero padding up to the next multiple of 256; CTA 0 stores h to hout.
+// Rows are processed in batches: every load of a batch (residual, norm
+// weight, up to four partials per row) is issued before any is used, so a
+// batch costs one round trip; h and w wait in shared memory (`tmp`, the idle
+// K/V page buffer) for the block-wide sum of squares.
 SR_DEV void mk_norm_prologue(const MkParams& p, int mode, int tok, const float* hin,
                              const float* part, const uint16_t* tab, const __nv_bfloat16* w,
-                             float* hout, __nv_bfloat16* xs, float* red, int c, int G) {
+                             float* hout, __nv_bfloat16* xs, float* red, int c, int G,
+                             float* tmp) {
   const int d = p.d, tid = threadIdx.x;
-  float hv[kMkNorm], wv[kMkNorm];
+  float* hs = tmp;                                            // [d] fp32
+  __nv_bfloat16* wsm = reinterpret_cast<__nv_bfloat16*>(tmp + d);  // [d] bf16
   float ss = 0.f;
+  constexpr int kNB = 4;
+  const size_t cs = (size_t)p.maxj * kTR;
+#pragma unroll 1
+  for (int i0 = tid; i0 < d; i0 += kNB * kMkConsumers) {
+    float hb[kNB], pb[kNB][4];
+    __nv_bfloat16 wb[kNB];
+    int nb[kNB];
 #pragma unroll
-  for (int j = 0; j < kMkNorm; ++j) {
-    const int i = tid + j * kMkConsumers;
-    float v = 0.f, wj = 0.f;
-    if (i < d) {
-      wj = bf_to_f(w[i]);  // issued with the vector loads: one round trip in all
-      if (mode == 0)
-        v = bf_to_f(p.embed[(size_t)tok * d + i]);
-      else
-        v = __ldcg(hin + i) + mk_sum_parts(part, tab, i, p.maxj);
+    for (int jj = 0; jj < kNB; ++jj) {
+      const int i = i0 + jj * kMkConsumers;
+      const bool ok = i < d;
+      const int ic = ok ? i : 0;
+      wb[jj] = w[ic];
+      if (mode == 0) {
+        hb[jj] = bf_to_f(p.embed[(size_t)tok * d + ic]);
+        nb[jj] = 0;
+        pb[jj][0] = pb[jj][1] = pb[jj][2] = pb[jj][3] = 0.f;
+      } else {
+        hb[jj] = __ldcg(hin + ic);
+        const int e = tab[ic / kTR];
+        const int r = ic % kTR;
+        const int c0 = e & 0xff, n = (e >> 8) & 0xf, jo = e >> 12;
+        const float* q1 = part + (size_t)(c0 + 1) * cs + r;
+        pb[jj][0] = __ldcg(part + (size_t)c0 * cs + (size_t)jo * kTR + r);
+        pb[jj][1] = n > 1 ? __ldcg(q1) : 0.f;
+        pb[jj][2] = n > 2 ? __ldcg(q1 + cs) : 0.f;
+        pb[jj][3] = n > 3 ? __ldcg(q1 + 2 * cs) : 0.f;
+        nb[jj] = n;
+      }
     }
-    hv[j] = v;
-    wv[j] = wj;
-    ss += v * v;
+#pragma unroll
+    for (int jj = 0; jj < kNB; ++jj) {
+      const int i = i0 + jj * kMkConsumers;
+      if (i < d) {
+        float v = hb[jj];
+        if (mode != 0) {
+          float sp = ((pb[jj][0] + pb[jj][1]) + pb[jj][2]) + pb[jj][3];
+          if (nb[jj] > 4) {  // tiny models only: more contributors than a batch holds
+            const int e = tab[i / kTR];
+            for (int q = 4; q < nb[jj]; ++q)
+              sp += __ldcg(part + (size_t)((e & 0xff) + q) * cs + i % kTR);
+          }
+          v += sp;
+        }
+        hs[i] = v;
+        wsm[i] = wb[jj];
+        ss += v * v;
+      }
+    }
   }
-  ss = cblock_sum(ss, red);
+  ss = cblock_sum(ss, red);  // (its barriers also publish hs / wsm)
   const float rstd = rsqrtf(ss / d + p.eps);
   const int dpad = (d + kTC - 1) / kTC * kTC;
-#pragma unroll
-  for (int j = 0; j < kMkNorm; ++j) {
-    const int i = tid + j * kMkConsumers;
-    if (i < d) {
-      xs[i] = __float2bfloat16_rn(hv[j] * rstd * wv[j]);
-      if (c == 0 && hout) hout[i] = hv[j];
-    }
+  for (int i = tid; i < d; i += kMkConsumers) {
+    const float v = hs[i];
+    xs[i] = __float2bfloat16_rn(v * rstd * bf_to_f(wsm[i]));
+    if (c == 0 && hout) hout[i] = v;
   }
   for (int i = d + tid; i < dpad; i += kMkConsumers) xs[i] = __float2bfloat16_rn(0.f);
   cbar();
@@ -268,7 +313,9 @@ SR_DEV void mk_gemv(const MkParams& p, const PhaseInfo& pi, int c, const uint8_t
   const int row_bytes = tc * 2;
   const bool active = lane * 8 < tc;
   int b = pi.b0, k = pi.k0;
-  float a0 = 0.f, a1 = 0.f;
+  float a[kRW];
+#pragma unroll
+  for (int i = 0; i < kRW; ++i) a[i] = 0.f;
   for (int u0 = lo; u0 < hi; u0 += kUPS) {
     mbar_wait(&full[rp.slot], rp.par);
     const uint8_t* stage = ring + (size_t)rp.slot * kStageBytes;
@@ -279,11 +326,12 @@ SR_DEV void mk_gemv(const MkParams& p, const PhaseInfo& pi, int c, const uint8_t
         const int u = u0 + q;
         if (active) {
           const uint8_t* tile = stage + q * kTileBytes;
-          const uint4 w0 = *reinterpret_cast<const uint4*>(tile + warp * row_bytes + lane * 16);
-          const uint4 w1 = *reinterpret_cast<const uint4*>(tile + (warp + 16) * row_bytes + lane * 16);
           const uint4 xv = *reinterpret_cast<const uint4*>(xs + k * tc + lane * 8);
-          a0 = dot8(w0, xv, a0);
-          a1 = dot8(w1, xv, a1);
+#pragma unroll
+          for (int i = 0; i < kRW; ++i) {
+            const uint4 w = *reinterpret_cast<const uint4*>(tile + (warp + i * kMkWarps) * row_bytes + lane * 16);
+            a[i] = dot8(w, xv, a[i]);
+          }
         }
         if (q == nu - 1) {  // stage fully read: hand it back to the producer
           __syncwarp();
@@ -291,23 +339,31 @@ SR_DEV void mk_gemv(const MkParams& p, const PhaseInfo& pi, int c, const uint8_t
           rp.advance(S);
         }
         if (k == kt - 1 || u == hi - 1) {
-          a0 = warp_sum(a0);
-          a1 = warp_sum(a1);
+#pragma unroll
+          for (int i = 0; i < kRW; ++i) a[i] = warp_sum(a[i]);
           if (lane == 0) {
             if constexpr (PH == PH_QKV || PH == PH_O || PH == PH_D) {
               float* part = PH == PH_QKV ? p.part_qkv : PH == PH_O ? p.part_o : p.part_d;
               float* dst = part + ((size_t)c * p.maxj + (b - pi.b0)) * kTR;
-              dst[warp] = a0;
-              dst[warp + 16] = a1;
+#pragma unroll
+              for (int i = 0; i < kRW; ++i) dst[warp + i * kMkWarps] = a[i];
             } else if constexpr (PH == PH_GU) {
-              p.act[b * 16 + warp] = __float2bfloat16_rn(a0 / (1.f + __expf(-a0)) * a1);
+              // rows warp + i*W (< 16) are gate units, +16 their up rows
+#pragma unroll
+              for (int i = 0; i < kRW / 2; ++i) {
+                const float g = a[i], up = a[i + kRW / 2];
+                p.act[b * 16 + warp + i * kMkWarps] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * up);
+              }
             } else {
-              const int r0 = b * kTR + warp;
-              if (r0 < p.vocab_text) best.push(a0, r0);
-              if (r0 + 16 < p.vocab_text) best.push(a1, r0 + 16);
+#pragma unroll
+              for (int i = 0; i < kRW; ++i) {
+                const int r = b * kTR + warp + i * kMkWarps;
+                if (r < p.vocab_text) best.push(a[i], r);
+              }
             }
           }
-          a0 = a1 = 0.f;
+#pragma unroll
+          for (int i = 0; i < kRW; ++i) a[i] = 0.f;
         }
         if (++k == kt) {
           k = 0;
@@ -352,10 +408,10 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
   float* mrun = alph + kMkMaxGq;               // [8]
   float* lrun = mrun + kMkMaxGq;               // [8]
   float* red = lrun + kMkMaxGq;                // [4][8][128]
-  float* kn = red + 4 * kMkMaxGq * 128;        // [128] new k (rotated, bf16 values)
+  float* kn = red + kGroups * kMkMaxGq * 128;  // [128] new k (rotated, bf16 values)
   float* vn = kn + 128;                        // [128] new v
   const float scale = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
-  const int posl = warp * 4 + (lane >> 3), sub = lane & 7;
+  const int sub = lane & 7;
   const int dd = tid % kHeadDim, grp = tid / kHeadDim;
 
   const bool sub_prof = p.prof && c == 0 && tid == 0 && layer == 1;
@@ -419,7 +475,9 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
     kvpar ^= 1u;
     SUB_EV();  // page landed
     // scores: 8 lanes per position, 16 dims per lane
-    {
+#pragma unroll
+    for (int pass = 0; pass < 64 / kPosPass; ++pass) {
+      const int posl = pass * kPosPass + warp * 4 + (lane >> 3);
       float sc[kMkMaxGq];
 #pragma unroll
       for (int j = 0; j < kMkMaxGq; ++j) sc[j] = 0.f;
@@ -488,26 +546,26 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
     }
     cbar();
     {
-      float vf[16];
+      float vf[kPPG];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) vf[q] = bf_to_f(vs[(grp * 16 + q) * kHeadDim + dd]);
-      if (newl >= grp * 16 && newl < grp * 16 + 16) {
+      for (int q = 0; q < kPPG; ++q) vf[q] = bf_to_f(vs[(grp * kPPG + q) * kHeadDim + dd]);
+      if (newl >= grp * kPPG && newl < grp * kPPG + kPPG) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (grp * 16 + q == newl) vf[q] = vn[dd];
+        for (int q = 0; q < kPPG; ++q)
+          if (grp * kPPG + q == newl) vf[q] = vn[dd];
       }
 #pragma unroll
       for (int j = 0; j < kMkMaxGq; ++j)
         if (j < Gq) acc[j] *= alph[j];
 #pragma unroll
-      for (int q = 0; q < 16; ++q)
-        if (grp * 16 + q >= nval) vf[q] = 0.f;  // slots past the context may hold garbage
+      for (int q = 0; q < kPPG; ++q)
+        if (grp * kPPG + q >= nval) vf[q] = 0.f;  // slots past the context may hold garbage
 #pragma unroll
       for (int j = 0; j < kMkMaxGq; ++j) {
         if (j < Gq) {
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const float4 pp = *reinterpret_cast<const float4*>(ps + j * 64 + grp * 16 + q4 * 4);
+          for (int q4 = 0; q4 < kPPG / 4; ++q4) {
+            const float4 pp = *reinterpret_cast<const float4*>(ps + j * 64 + grp * kPPG + q4 * 4);
             acc[j] = fmaf(pp.x, vf[4 * q4], acc[j]);
             acc[j] = fmaf(pp.y, vf[4 * q4 + 1], acc[j]);
             acc[j] = fmaf(pp.z, vf[4 * q4 + 2], acc[j]);
@@ -525,8 +583,9 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
   cbar();
   if (grp == 0) {
     for (int j = 0; j < Gq; ++j) {
-      const float o = red[(0 * kMkMaxGq + j) * 128 + dd] + red[(1 * kMkMaxGq + j) * 128 + dd] +
-                      red[(2 * kMkMaxGq + j) * 128 + dd] + red[(3 * kMkMaxGq + j) * 128 + dd];
+      float o = 0.f;
+#pragma unroll
+      for (int g2 = 0; g2 < kGroups; ++g2) o += red[(g2 * kMkMaxGq + j) * 128 + dd];
       p.apart[((size_t)c * kMkMaxGq + j) * 130 + dd] = o;
     }
   }
@@ -676,6 +735,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = mk_smem;
   uint8_t* kvbuf = mk_smem + (size_t)S * kStageBytes;  // one K page + one V page
+  float* kvtmp = reinterpret_cast<float*>(kvbuf);         // prologue scratch (d <= 5120)
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(kvbuf + kKvBufBytes);
   float* scratch = reinterpret_cast<float*>(xs);
 
@@ -800,9 +860,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       const MkLayer ly = p.layers[l];
       // QKV
       if (l == 0)
-        mk_norm_prologue(p, 0, tok, nullptr, nullptr, s_tab[2], ly.ln1, p.hA, xs, red, c, G);
+        mk_norm_prologue(p, 0, tok, nullptr, nullptr, s_tab[2], ly.ln1, p.hA, xs, red, c, G, kvtmp);
       else
-        mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], ly.ln1, p.hA, xs, red, c, G);
+        mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], ly.ln1, p.hA, xs, red, c, G, kvtmp);
       MK_EV();  // 1 qkv prologue
       mk_gemv<PH_QKV>(p, s_ph[PH_QKV], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 2 qkv gemv
@@ -833,7 +893,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 10 sync
       // gate / up
-      mk_norm_prologue(p, 1, tok, p.hA, p.part_o, s_tab[1], ly.ln2, p.hB, xs, red, c, G);
+      mk_norm_prologue(p, 1, tok, p.hA, p.part_o, s_tab[1], ly.ln2, p.hB, xs, red, c, G, kvtmp);
       MK_EV();  // 11 prologue
       mk_gemv<PH_GU>(p, s_ph[PH_GU], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 12 gu gemv
@@ -848,7 +908,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       MK_EV();  // 16 sync
     }
     // LM head + greedy argmax
-    mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], p.ln_f, nullptr, xs, red, c, G);
+    mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], p.ln_f, nullptr, xs, red, c, G, kvtmp);
     MK_EV();
     mk_gemv<PH_LM>(p, s_ph[PH_LM], c, ring, full, empty, xs, rp, S, best);
     MK_EV();
