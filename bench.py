@@ -445,7 +445,9 @@ def main() -> None:
         faulthandler.dump_traceback_later(int(os.environ["BENCH_STACK_DUMP_S"]), repeat=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=60)
+    # the loop's step mix (draft steps accepted or regenerated) varies a lot
+    # between random-init trajectories: 120 steps span several of them
+    ap.add_argument("--steps", type=int, default=120)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pair", default="1.5b+7b")

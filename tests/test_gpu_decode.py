@@ -129,3 +129,22 @@ def test_full_size_draft_decode_replays_on_oracle(cuda):
         if t == top:
             top2 = torch.topk(lg[k], 2).values
             assert abs(float(top2[0] - top2[1]) - margins[k]) < tol
+
+
+def test_persistent_kernel_long_context(cuda):
+    """Several K/V pages per attention split (long CoT): the persistent
+    kernel against the per-kernel graph decode at ~6K context."""
+    spec = get_spec("tiny-base")
+    w = make_weights(spec, 0)
+    v = shared_vocab(spec.vocab_text)
+    mk = _backend(spec, w, max_ctx=8192)
+    gr = _backend(spec, w, "graph", max_ctx=8192)
+    ref = RefEngine(spec, w, v)
+    g = torch.Generator().manual_seed(3)
+    ctx = torch.randint(16, v.n_text, (6000,), generator=g).tolist()
+    a, _ = mk.engine.generate(mk.pool.streams[0], ctx, 24, ())
+    b, _ = gr.engine.generate(gr.pool.streams[0], ctx, 24, ())
+    if a != b:
+        k = next(i for i, (x, y) in enumerate(zip(a, b)) if x != y)
+        lg = ref.logits_teacher_forced(ctx + a[:k])[-1][: v.n_text]
+        assert abs(float(lg[a[k]] - lg[b[k]])) < 5e-2, k

@@ -1,4 +1,3 @@
-timeout 300 python -m pytest tests/test_gpu_decode.py tests/test_gpu_parity.py -x -q 2>&1 | tail -1
-for m in r1-1.5b qwen2.5-7b qwq-32b; do
-timeout 300 python tools/mk_prof.py $m --ctx 2048 > gpurun_out/mkprof_$m.log 2>&1
-done
+timeout 600 python -m pytest tests/test_gpu_decode.py -x -q -k long 2>&1 | tail -3
+timeout 900 python bench.py --steps 30 --warmup 3 > gpurun_out/bench_c2.log 2>&1
+tail -1 gpurun_out/bench_c2.log | cut -c1-400
