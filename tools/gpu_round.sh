@@ -1,3 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_decode.py -x -q -k long 2>&1 | tail -3
-timeout 900 python bench.py --steps 30 --warmup 3 > gpurun_out/bench_c2.log 2>&1
-tail -1 gpurun_out/bench_c2.log | cut -c1-400
+timeout 1200 python bench.py > gpurun_out/bench_default.log 2>&1
+tail -1 gpurun_out/bench_default.log | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['breakdown_ms_per_step'], d['loop'], d['roofline']['frac'], d['e2e']['value'], d['cpu_baseline']['value'])"
