@@ -184,6 +184,7 @@ def run_ours(args) -> None:
         base_tp = TensorParallel.from_dist() if dist is not None else TensorParallel.single()
     small, base = build_pair(args.pair, seed=args.seed, max_ctx=args.budget + 512,
                              threshold=args.threshold, base_tp=base_tp)
+    base.verify_template = args.verify_template
     if args.spec_gamma > 0:  # SpecReason+Decode: the draft proposes tokens inside base fallback
         base.attach_speculator(small, gamma=args.spec_gamma)
     vocab = shared_vocab(get_spec(PAIRS[args.pair][0]).vocab_text)
@@ -244,6 +245,7 @@ def run_ours(args) -> None:
         "dtype": "bf16",
         "data": "synthetic (random-init weights, seeded 64-word problems)",
         "config": {"workload": WORKLOADS[args.pair], "pair": args.pair, "threshold": args.threshold,
+                   "verify_template": args.verify_template, "spec_gamma": args.spec_gamma,
                    "token_budget": args.budget, "max_step_tokens": args.max_step_tokens,
                    "batch": 1, "parallelism": (f"dp{world} (independent problems per GPU)"
                                                if args.mode == "dp" else
@@ -457,6 +459,8 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-layers", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verify-template", default="v1", choices=["v1", "v2"],
+                    help="v2: prefix-sharing verification prompt (not the reference wording)")
     ap.add_argument("--spec-gamma", type=int, default=0,
                     help="token-level speculation inside base generation (0 = off)")
     ap.add_argument("--mode", default="dp", choices=["dp", "tp"],

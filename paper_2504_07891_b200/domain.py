@@ -411,6 +411,25 @@ VERIFY_PROMPT_V1 = (
 )
 
 
+# Prefix-sharing verification template (not the reference's
+# wording, so scores are not comparable with VERIFY_PROMPT_V1 and it is
+# opt-in).  It starts with the generation prompt itself -- problem, the think
+# marker, the CoT -- and appends the candidate as the next step, so the base
+# model's generation stream already holds the K/V of everything but the
+# candidate and the short tail, and an accepted candidate's K/V stays in place
+# for the next step.  The last word is the same judge cue as V1's.
+VERIFY_PROMPT_V2_TAIL = (
+    "\n\nJudge only the last step above. A high score means the step is correct,\n"
+    "relevant, and moves the reasoning forward; a low score means it is wrong,\n"
+    "redundant, or off-track.\n"
+    "Respond with a single digit 0-9:"
+)
+
+
+def render_verification_prompt_v2(problem: str, cot_prefix: str, candidate_step: str) -> str:
+    return render_generation_prompt(problem, cot_prefix) + candidate_step + VERIFY_PROMPT_V2_TAIL
+
+
 def render_verification_prompt(problem: str, cot_prefix: str, candidate_step: str,
                                template: str = VERIFY_PROMPT_V1) -> str:
     return template.format(problem=problem, cot_prefix=cot_prefix,

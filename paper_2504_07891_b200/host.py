@@ -201,6 +201,7 @@ class ModelBackend(Backend):
         self._prompts = _PromptCache(vocab)
         self.record = record
         self.calls: list[dict] = []   # per-call trace (ids) for replay parity
+        self.verify_template = "v1"   # "v2": prefix-sharing verification prompts
 
     # -- token-level speculation (SpecReason+Decode) ----------
     def attach_speculator(self, draft: "ModelBackend", gamma: int = 5) -> None:
@@ -299,8 +300,12 @@ class ModelBackend(Backend):
         T = self.types
         if self.profile.role != T.BackendRole.BASE:
             raise ValueError(f"backend {self.profile.name} cannot score steps")
-        prompt = T.render_verification_prompt(request.problem, request.cot_prefix,
-                                              request.candidate_step)
+        if self.verify_template == "v2":  # prefix-sharing (opt-in; §8f-3)
+            prompt = domain.render_verification_prompt_v2(request.problem, request.cot_prefix,
+                                                          request.candidate_step)
+        else:
+            prompt = T.render_verification_prompt(request.problem, request.cot_prefix,
+                                                  request.candidate_step)
         with self._lock:
             ids = self._prompts.encode(prompt)
             stream, keep = self.pool.acquire(ids)

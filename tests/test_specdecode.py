@@ -70,3 +70,26 @@ def test_speculative_generation_is_lossless(tiny_vocab, draft_name):
         assert rate > 0.9, st
     else:
         assert rate < 0.5, st
+
+
+def test_prefix_sharing_verify_template_reuses_the_generation_stream(tiny_vocab):
+    """§8f-3: with the v2 template the verification prompt extends the
+    generation prompt, so a trajectory prefills far fewer base tokens; the
+    engine's invariants still hold."""
+    from paper_2504_07891_b200 import AcceptanceThreshold, EngineConfig, run_trajectory
+    from paper_2504_07891_b200.domain import render_verification_prompt_v2
+    from paper_2504_07891_b200.driver import validate_trajectory
+
+    prompt = render_verification_prompt_v2("p q", "a b. ", "c d. ")
+    assert prompt.startswith(render_generation_prompt("p q", "a b. ")) and prompt.endswith("0-9:")
+    fresh = {}
+    for tmpl in ("v1", "v2"):
+        small = oracle_backend("tiny-draft", BackendRole.SMALL)
+        base = oracle_backend("tiny-base", BackendRole.BASE, record=True)
+        base.verify_template = tmpl
+        cfg = EngineConfig(threshold=AcceptanceThreshold(7), temperature=0.0,
+                           max_step_tokens=32, token_budget=256)
+        res = run_trajectory(cfg, tiny_vocab.problem(64, 2), small, base)
+        validate_trajectory(res, cfg)
+        fresh[tmpl] = sum(c["fresh"] for c in base.calls)
+    assert fresh["v2"] < 0.9 * fresh["v1"], fresh
