@@ -56,6 +56,7 @@ def own_types() -> SimpleNamespace:
                            UtilityScore=domain.UtilityScore,
                            ScoreParseFailure=contract.ScoreParseFailure,
                            BackendMisbehavior=contract.BackendMisbehavior,
+                           TransportError=contract.TransportError,
                            BackendProfile=domain.BackendProfile,
                            BackendRole=domain.BackendRole,
                            render_verification_prompt=domain.render_verification_prompt)
@@ -74,6 +75,7 @@ def reference_types(stepspec: Any) -> SimpleNamespace:
                            UtilityScore=core.UtilityScore,
                            ScoreParseFailure=base.ScoreParseFailure,
                            BackendMisbehavior=base.BackendMisbehavior,
+                           TransportError=base.TransportError,
                            BackendProfile=core.BackendProfile,
                            BackendRole=core.BackendRole,
                            render_verification_prompt=prompts.render_verification_prompt)
@@ -262,8 +264,34 @@ class ModelBackend(Backend):
                 if done:
                     return out, finish
 
+    def _device_error(self, exc: Exception):
+        """Map a native failure onto the reference's error hierarchy
+        (base.py:19-32): collectives (NCCL) -> TransportError, everything
+        else on the device -> BackendMisbehavior; the engine then adds the
+        "step N of problem" context (engine.py:269-273)."""
+        T = self.types
+        code = getattr(exc, "code", None)
+        cls = T.TransportError if code == 1004 else T.BackendMisbehavior
+        return cls(f"{self.profile.name}: {exc}")
+
     # -- API -------------------------------------------------------------
     def generate_step(self, request: GenerationRequest):
+        try:
+            return self._generate_step(request)
+        except RuntimeError as exc:
+            if type(exc).__name__ != "NativeError":
+                raise
+            raise self._device_error(exc) from exc
+
+    def score_step(self, request: VerificationRequest):
+        try:
+            return self._score_step(request)
+        except RuntimeError as exc:
+            if type(exc).__name__ != "NativeError":
+                raise
+            raise self._device_error(exc) from exc
+
+    def _generate_step(self, request: GenerationRequest):
         if not request.prompt:
             raise ValueError("prompt must be non-empty")
         t0 = time.monotonic()
@@ -296,7 +324,7 @@ class ModelBackend(Backend):
         return T.GenerationResult(text=text, token_count=len(text_ids), finish_reason=reason,
                                   measured_latency_s=time.monotonic() - t0)
 
-    def score_step(self, request: VerificationRequest):
+    def _score_step(self, request: VerificationRequest):
         T = self.types
         if self.profile.role != T.BackendRole.BASE:
             raise ValueError(f"backend {self.profile.name} cannot score steps")

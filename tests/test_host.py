@@ -178,3 +178,42 @@ def test_cabi_rejects_bad_descriptor():
                          max_tokens=4, max_new=4, n_pages=1)
     assert lib.sr_workspace_bytes(ctypes.byref(d)) == 0
     assert b"d_model" in lib.sr_last_error()
+
+
+def test_native_errors_map_onto_the_reference_hierarchy(tiny_vocab):
+    """Device failures surface as BackendMisbehavior (collectives as
+    TransportError), so the engine adds the step context (engine.py:269-273)."""
+    import pytest
+
+    from paper_2504_07891_b200 import contract
+    from paper_2504_07891_b200.contract import GenerationRequest, VerificationRequest
+    from paper_2504_07891_b200.domain import BackendProfile, BackendRole
+    from paper_2504_07891_b200.host import ModelBackend
+    from paper_2504_07891_b200.native import NativeError
+
+    class Failing:
+        spec = None
+
+        def __init__(self, code):
+            self.code = code
+
+        def attach(self, stream):
+            stream.handle = None
+
+        def truncate(self, stream, keep):
+            del stream.ids[keep:]
+
+        def generate(self, *a):
+            raise NativeError("sr_generate", self.code, "boom")
+
+        def score(self, *a):
+            raise NativeError("sr_score", self.code, "boom")
+
+    prof = BackendProfile(name="x", role=BackendRole.BASE, decode_s_per_token=1e-3,
+                          prefill_tokens_per_s=1e3)
+    b = ModelBackend(Failing(700), tiny_vocab, prof)
+    with pytest.raises(contract.BackendMisbehavior):
+        b.generate_step(GenerationRequest(prompt="a b ", max_tokens=4))
+    t = ModelBackend(Failing(1004), tiny_vocab, prof)
+    with pytest.raises(contract.TransportError):
+        t.score_step(VerificationRequest("a", "b ", "c "))
