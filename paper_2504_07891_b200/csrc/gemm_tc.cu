@@ -467,8 +467,17 @@ int tc_token_tile(int M) {
   return t < cap ? t : cap;
 }
 
-int tc_pick_splits(int M, int N, int K, int num_sms) {
-  const int nt = tc_token_tile(M);
+// narrow-N GEMMs (O, down: N = d) with long token runs: 256-token tiles would
+// leave most SMs idle (7B at M = 640: 84 tiles for 148 SMs); 128-token tiles
+// double the tile count and run two CTAs per SM
+int tc_pick_tile(int M, int N, int num_sms) {
+  int nt = tc_token_tile(M);
+  if (nt == 256 && (long)((N + kWRows - 1) / kWRows) * ((M + 255) / 256) < num_sms) nt = 128;
+  return nt;
+}
+
+int tc_pick_splits(int M, int N, int K, int num_sms, int nt_in) {
+  const int nt = nt_in ? nt_in : tc_token_tile(M);
   const int tiles = ((N + kWRows - 1) / kWRows) * ((M + nt - 1) / nt);
   const int nkb = K / kBK;
   // token tiles <= 128 run a 3-stage ring, two CTAs per SM: fill both slots
@@ -579,7 +588,7 @@ static cudaError_t launch_nt(const TcGemmArgs& a, cudaStream_t stream) {
 
 cudaError_t gemm_tc_launch(const TcGemmArgs& a, cudaStream_t stream) {
   if (a.K % kBK != 0) return cudaErrorInvalidValue;
-  switch (tc_token_tile(a.M)) {
+  switch (a.nt ? a.nt : tc_token_tile(a.M)) {
     case 32: return launch_nt<32>(a, stream);
     case 64: return launch_nt<64>(a, stream);
     case 96: return launch_nt<96>(a, stream);

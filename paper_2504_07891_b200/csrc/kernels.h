@@ -127,12 +127,14 @@ struct TcGemmArgs {
   int M, N, K, splits;
   __nv_bfloat16* act;  // non-null (splits == 1, interleaved gate/up W): write
                        // bf16 silu(gate) * up [M, N/2] instead of C
+  int nt;              // token tile (0: tc_token_tile(M))
 };
+int tc_pick_tile(int M, int N, int num_sms);
 int make_tmap_bf16(void* out_map, const void* ptr, int rows, int cols, int box_rows);
 int make_tmap_bf16_box(void* out_map, const void* ptr, int rows, int cols, int box_cols,
                        int box_rows, bool swizzle128);
 int tc_token_tile(int M);
-int tc_pick_splits(int M, int N, int K, int num_sms);
+int tc_pick_splits(int M, int N, int K, int num_sms, int nt = 0);
 cudaError_t gemm_tc_launch(const TcGemmArgs& a, cudaStream_t stream);
 
 struct EpiParams {

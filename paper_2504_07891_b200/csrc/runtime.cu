@@ -609,7 +609,8 @@ struct Model {
     if (use_tc) {
       TcGemmArgs a{};
       a.act = glu_out;
-      const int nt = tc_token_tile(M);
+      const int nt = tc_pick_tile(M, N, num_sms);
+      a.nt = nt;
       const int ti = nt == 32 ? 0 : nt == 64 ? 1 : nt == 96 ? 2 : nt == 128 ? 3 : 4;
       a.tmW = &wmaps[wmap].m;
       a.tmX = &amaps[act_id][ti].m;
@@ -617,7 +618,7 @@ struct Model {
       a.M = M;
       a.N = N;
       a.K = K;
-      int sp = tc_pick_splits(M, N, K, num_sms);
+      int sp = tc_pick_splits(M, N, K, num_sms, nt);
       while (sp > 1 && (size_t)sp * M * N > L.part_floats) --sp;
       a.splits = sp;
       last_splits = sp;
