@@ -106,6 +106,12 @@ cudaError_t attn_tc_launch(const AttnParams& p, int M_tokens, int nsplit, cudaSt
 int attn_tc_splits(int n_kv, int q_tiles, int T, int num_sms);
 cudaError_t attn_merge_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream);
 cudaError_t attn_prefill_launch(const AttnParams& p, int M, cudaStream_t stream);
+// tcgen05 flash attention (attention_umma.cu); tmK / tmV: 128-B swizzled tensor
+// maps over the K / V pools viewed as [rows = L*n_pages*n_kv*64, 128], box 64x64
+cudaError_t attn_umma_launch(const void* tmK, const void* tmV, const AttnParams& p, int M_tokens,
+                             int nsplit, cudaStream_t stream);
+int attn_umma_splits(int n_kv, int q_tiles, int T, int num_sms);
+int attn_umma_q_tiles(int M_tokens, int G);
 
 // ----------------------------------------------------------- prefill path ---
 // C_partial[s][m][n] = sum_{k in split s} A[m][k] * B[n][k]

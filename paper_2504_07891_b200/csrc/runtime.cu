@@ -134,10 +134,12 @@ struct Model {
   float *tp_send, *tp_gather, *tp_dig, *tp_dec;
   int* tp_counts;
   bool attn_simt = false;      // SR_ATTN=simt: CUDA-core split-KV attention (A/B reference)
+  bool attn_umma = true;       // tcgen05 prefill attention; SR_ATTN=tc: mma.sync (A/B)
   bool prefetch = false;       // SR_PREFETCH=1: GEMV L2 prefetch before the PDL wait
   struct alignas(64) TMap { CUtensorMap m; };
   std::vector<TMap> wmaps;     // per layer: qkv, o, gu, d ; then lm_head
   TMap amaps[3][5];            // [x | attn | act][token tile 32/64/96/128/256]
+  TMap kvmaps[2];              // K / V pools as [L*n_pages*n_kv*64, 128], 64x64 boxes
   enum { ACT_X = 0, ACT_ATTN = 1, ACT_ACT = 2 };
 
   int build_tmaps() {
@@ -159,6 +161,12 @@ struct Model {
       for (int t = 0; t < 5; ++t)
         if (make_tmap_bf16(&amaps[i][t].m, a[i], d.max_tokens, acols[i], tiles[t]))
           return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for an activation");
+    const long kv_rows = (long)d.n_layers * d.n_pages * d.n_kv_heads * SR_PAGE;
+    if (kv_rows >= (1L << 31)) return fail(SR_E_INVALID, "K/V pool too large for a tensor map");
+    const void* pools[2] = {k_pool, v_pool};
+    for (int i = 0; i < 2; ++i)
+      if (make_tmap_bf16_box(&kvmaps[i].m, pools[i], (int)kv_rows, SR_HEAD_DIM, 64, SR_PAGE, true))
+        return fail(SR_E_INVALID, "cuTensorMapEncodeTiled failed for a K/V pool");
     return 0;
   }
 
@@ -444,6 +452,13 @@ struct Model {
         if (attn_simt) {
           a.nsplit = std::min(kAttnPrefillSplit, attn_prefill_splits(Tlast));
           SR_CK(attn_prefill_launch(a, M, s));
+        } else if (attn_umma) {
+          const int G = d.n_heads / d.n_kv_heads;
+          a.nsplit = std::min(kAttnPrefillSplit,
+                              attn_umma_splits(d.n_kv_heads, attn_umma_q_tiles(M, G), Tlast, num_sms));
+          SR_CK(attn_umma_launch(&kvmaps[0].m, &kvmaps[1].m, a, M, a.nsplit, s));
+          if (a.nsplit > 1) SR_CK(attn_merge_launch(a, M, a.nsplit, s));
+          watch(s, "attn_prefill_umma", l, M, a.nsplit);
         } else {
           const int G = d.n_heads / d.n_kv_heads;
           const int q_tiles = (M * G + 63) / 64;
@@ -758,7 +773,10 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
     m->stream_decode = strcmp(v, "stream") == 0;
     m->graph_decode = strcmp(v, "graph") == 0;
   }
-  if (const char* v = getenv("SR_ATTN")) m->attn_simt = strcmp(v, "simt") == 0;
+  if (const char* v = getenv("SR_ATTN")) {
+    m->attn_simt = strcmp(v, "simt") == 0;
+    m->attn_umma = strcmp(v, "tc") != 0 && !m->attn_simt;
+  }
   if (const char* v = getenv("SR_PREFETCH")) m->prefetch = v[0] == '1';
   if (const char* v = getenv("SR_ATTN_PHI")) m->p_hi_only = v[0] == '1';
   if (const char* v = getenv("SR_WATCH")) {

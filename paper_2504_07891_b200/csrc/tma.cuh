@@ -93,4 +93,57 @@ SR_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// ----------------------------------------------------------- tcgen05 ---
+// UMMA shared-memory descriptor: K-major, 128-B swizzle, 8-row groups 1024 B apart
+SR_DEV uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major) = 1
+  d |= (uint64_t)(1024 >> 4) << 32;              // SBO = 1024 B
+  d |= (uint64_t)1 << 46;                        // version (sm100)
+  d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: bf16 x bf16 -> fp32, both K-major, M=128, N=n
+SR_DEV uint32_t umma_idesc(int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;                       // D = f32
+  d |= 1u << 7;                       // A = bf16
+  d |= 1u << 10;                      // B = bf16
+  d |= (uint32_t)(n >> 3) << 17;      // N
+  d |= (uint32_t)(128 >> 4) << 24;    // M = 128
+  return d;
+}
+
+SR_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                      uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+SR_DEV void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+
+// UMMA descriptor for an MN-major operand in 128-B swizzled 8-row atoms: MN
+// runs of 64 bf16 (128 B) per row, 8 K-rows per 1024-B atom (SBO), the next
+// 64-wide MN chunk `lbo_bytes` away (LBO)
+SR_DEV uint64_t umma_desc_sw128_mn(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 }  // namespace sr

@@ -56,6 +56,25 @@ def test_prefill_logits(sliced):
     assert err.max().item() <= TOL_MAX and err.mean().item() <= TOL_MEAN
 
 
+def test_prefill_logits_chunked_long(sliced):
+    """~1000 positions in 512-token chunks: the second chunk attends to a
+    16-page context (several pages per KV split, both TMEM S buffers and both
+    K/V stages reused), at the real GQA grouping."""
+    from paper_2504_07891_b200.backend import B200Backend
+
+    spec, _, ref, v = sliced
+    rng = np.random.default_rng(9)
+    ids = [int(x) for x in rng.integers(16, v.n_text, size=1000)]
+    gpu = B200Backend(spec, BackendRole.BASE, weights=make_weights(get_spec(spec.name), 0, layers=[0, 1]),
+                      max_ctx=1100, max_tokens=512)
+    s = gpu.pool.streams[0]
+    got = gpu.engine.forward_logits(s, ids).cpu()[:, : v.n_text]
+    want = ref.logits_teacher_forced(ids)[:, : v.n_text]
+    err = (got - want).abs()
+    print(f"{spec.name} 2L chunked: max-abs {err.max():.3e} mean-abs {err.mean():.3e} over {tuple(err.shape)}")
+    assert err.max().item() <= TOL_MAX and err.mean().item() <= TOL_MEAN
+
+
 def test_decode_replay(sliced):
     spec, gpu, ref, v = sliced
     ids = v.encode(render_generation_prompt(v.problem(64, 12), ""))
