@@ -31,7 +31,9 @@ constexpr int kFaHalf = 64 * 64 * 2;                 // one [64 x 64] bf16 sub-t
 constexpr int kFaStage = 4 * kFaHalf;                // K (2 halves) + V (2 halves): 32 KB
 constexpr int kFaQBytes = 2 * kFaRows * 128;         // Q: 2 x [128 x 64]: 32 KB
 constexpr int kFaStages = 2;                         // K/V pages in flight
-constexpr int kFaSmem = kFaQBytes + kFaStages * kFaStage + 1024;  // 97 KB: 2 CTAs / SM
+constexpr int kStageLd = 132;  // fp32 row pitch of the epilogue staging (bank spread)
+constexpr int kFaSmem = kFaQBytes + kFaStages * kFaStage + 1024;
+static_assert(kFaRows * kStageLd * 4 <= kFaQBytes + kFaStages * kFaStage, "epilogue staging fits");  // 97 KB: 2 CTAs / SM
 constexpr float kFaScaleLog2 = 1.4426950408889634f * 0.08838834764831845f;
 
 // byte offset of (row, 16-B chunk) in a 128-B-swizzled K-major [rows x 64] tile
@@ -328,17 +330,14 @@ __global__ void __launch_bounds__(kFaThreads, 2)
     l += xch[0][hf ^ 1][r];
     const int rr = row0 + r;
     const size_t part_stride = kHeadDim + 2;
-    __nv_bfloat16* orow = nullptr;
-    float* prow = nullptr;
-    if (r < rows_here) {
-      const int tok = rr / G, j = rr % G;
-      if (nsplit == 1)
-        orow = p.out + (size_t)tok * p.n_heads * kHeadDim + (size_t)(g * G + j) * kHeadDim;
-      else
-        prow = p.part + ((size_t)rr * nsplit + split) * part_stride +
-               (size_t)g * M_rows * nsplit * part_stride;
-    }
+    float* prow = nullptr;  // this row's (m, l) slot of the split partials
+    if (r < rows_here && nsplit > 1)
+      prow = p.part + ((size_t)rr * nsplit + split) * part_stride +
+             (size_t)g * M_rows * nsplit * part_stride;
     const float inv = l > 0.f ? 1.f / l : 0.f;
+    // O rows leave TMEM one per thread; they are staged through the (now idle)
+    // Q and K/V buffers so that each warp stores whole rows (coalesced)
+    float* stage = reinterpret_cast<float*>(sQ);  // [128 rows][kStageLd] fp32
 #pragma unroll
     for (int c = 64 * hf; c < 64 * hf + 64; c += 32) {
       float o[32];
@@ -348,14 +347,30 @@ __global__ void __launch_bounds__(kFaThreads, 2)
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = 0.f;  // empty split: (m, l, O) = (-inf, 0, 0)
       }
-      if (orow) {
+      const float sc = nsplit == 1 ? inv : 1.f;
 #pragma unroll
-        for (int e = 0; e < 32; e += 2)
-          *reinterpret_cast<uint32_t*>(orow + c + e) = f2_to_bf2(o[e] * inv, o[e + 1] * inv);
-      } else if (prow) {
+      for (int e = 0; e < 32; e += 4)
+        *reinterpret_cast<float4*>(stage + r * kStageLd + c + e) =
+            make_float4(o[e] * sc, o[e + 1] * sc, o[e + 2] * sc, o[e + 3] * sc);
+    }
+    named_barrier_sync(1, kFaSoftmaxWarps * 32);
+    const int lane = tid & 31;
+    for (int row = warp; row < rows_here; row += kFaSoftmaxWarps) {
+      const int rw = row0 + row;
+      const float* src = stage + row * kStageLd;
+      if (nsplit == 1) {
+        const int tok = rw / G, j = rw % G;
+        __nv_bfloat16* o =
+            p.out + (size_t)tok * p.n_heads * kHeadDim + (size_t)(g * G + j) * kHeadDim;
+        const float4 v = *reinterpret_cast<const float4*>(src + 4 * lane);
+        *reinterpret_cast<uint2*>(o + 4 * lane) = make_uint2(f2_to_bf2(v.x, v.y), f2_to_bf2(v.z, v.w));
+      } else {
+        float* dst = p.part + ((size_t)rw * nsplit + split) * part_stride +
+                     (size_t)g * M_rows * nsplit * part_stride;
 #pragma unroll
-        for (int e = 0; e < 32; e += 2)  // rows are 520 B apart: 8-B aligned
-          *reinterpret_cast<float2*>(prow + c + e) = make_float2(o[e], o[e + 1]);
+        for (int h = 0; h < 2; ++h)  // rows are 520 B apart: 8-B stores
+          *reinterpret_cast<float2*>(dst + 64 * h + 2 * lane) =
+              *reinterpret_cast<const float2*>(src + 64 * h + 2 * lane);
       }
     }
     if (prow && hf == 0) {
