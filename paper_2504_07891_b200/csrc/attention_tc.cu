@@ -368,35 +368,50 @@ __global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams
 // Split merge for prefill as its own grid-wide kernel: thread = (query row,
 // dim); fixed split order (deterministic).  A single last CTA per query tile
 // would read every split of 64 rows serially.
-__global__ void __launch_bounds__(512) attn_merge_kernel(AttnParams p, int M_rows, int G,
+__global__ void __launch_bounds__(256) attn_merge_kernel(AttnParams p, int M_rows, int G,
                                                          int nsplit) {
+  // warp = one (query row, kv head g); lane = 4 dims.  The (m, l) of all splits
+  // are loaded at once (lane sp holds split sp), then every split's 4 dims.
   grid_launch_dependents();
   grid_wait();
-  const int g = blockIdx.y;
-  const int r = blockIdx.x * 4 + (threadIdx.x >> 7), d = threadIdx.x & 127;
+  const int g = blockIdx.y, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (r >= M_rows) return;
   constexpr size_t ps = kHeadDim + 2;
   const float* base = p.part + (size_t)g * M_rows * nsplit * ps + (size_t)r * nsplit * ps;
-  float M = -INFINITY;
-  for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, base[sp * ps + kHeadDim]);
-  float L = 0.f, A = 0.f;
+  const float ms = lane < nsplit ? base[lane * ps + kHeadDim] : -INFINITY;
+  const float ls = lane < nsplit ? base[lane * ps + kHeadDim + 1] : 0.f;
+  float M = ms;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+  float L = w * ls;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int d = 2 * lane;  // dims d, d+1 and 64+d, 64+d+1 (rows are 8-B aligned)
 #pragma unroll 4
   for (int sp = 0; sp < nsplit; ++sp) {
-    const float ms = base[sp * ps + kHeadDim];
-    const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
-    L = fmaf(w, base[sp * ps + kHeadDim + 1], L);
-    A = fmaf(w, base[sp * ps + d], A);
+    const float ws = __shfl_sync(0xffffffffu, w, sp);
+    const float2 a = *reinterpret_cast<const float2*>(base + sp * ps + d);
+    const float2 b = *reinterpret_cast<const float2*>(base + sp * ps + 64 + d);
+    A.x = fmaf(ws, a.x, A.x);
+    A.y = fmaf(ws, a.y, A.y);
+    A.z = fmaf(ws, b.x, A.z);
+    A.w = fmaf(ws, b.y, A.w);
   }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
   __nv_bfloat16* o = const_cast<__nv_bfloat16*>(q_row_ptr(p, G, g, r)) - p.q + p.out;
-  o[d] = __float2bfloat16_rn(L > 0.f ? A / L : 0.f);
+  *reinterpret_cast<uint32_t*>(o + d) = f2_to_bf2(A.x * inv, A.y * inv);
+  *reinterpret_cast<uint32_t*>(o + 64 + d) = f2_to_bf2(A.z * inv, A.w * inv);
 }
 
 cudaError_t attn_merge_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream) {
   const int G = p.n_heads / p.n_kv;
   const int M_rows = M_tokens * G;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((M_rows + 3) / 4, p.n_kv);
-  cfg.blockDim = dim3(512);
+  cfg.gridDim = dim3((M_rows + 7) / 8, p.n_kv);
+  cfg.blockDim = dim3(256);
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
