@@ -53,6 +53,16 @@ struct Layout {  // workspace carve-up (byte offsets)
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+// CTAs of the persistent decode kernel: one per SM unless SR_MK_CTAS asks for
+// fewer (an experiment knob: fewer CTAs arrive at each grid barrier)
+static int mk_ctas_for(int num_sms) {
+  static const int v = [] {
+    const char* e = getenv("SR_MK_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  return v >= 16 && v < num_sms ? v : num_sms;
+}
+
 static Layout make_layout(const sr_model_desc& d, int num_sms) {
   Layout L{};
   const size_t T = d.max_tokens;
@@ -83,13 +93,14 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
   L.logits = take((size_t)d.vocab_rows * 4);
   L.ro_cnt = take(64);
   // persistent decode kernel (decode_mk.cu)
+  const int mk_g = mk_ctas_for(num_sms);
   const int qd_i = d.n_heads * SR_HEAD_DIM, qkv_i = qd_i + 2 * d.n_kv_heads * SR_HEAD_DIM;
-  L.mk_maxj = std::max({mk_max_j(qkv_i, d.d_model, num_sms), mk_max_j(d.d_model, qd_i, num_sms),
-                        mk_max_j(d.d_model, d.d_ffn, num_sms)});
+  L.mk_maxj = std::max({mk_max_j(qkv_i, d.d_model, mk_g), mk_max_j(d.d_model, qd_i, mk_g),
+                        mk_max_j(d.d_model, d.d_ffn, mk_g)});
   L.mk_maps = take(((size_t)d.n_layers * 4 + 1) * sizeof(CUtensorMap));
   L.mk_layers = take((size_t)d.n_layers * sizeof(MkLayer));
   L.mk_h = take(2 * (size_t)d.d_model * 4);
-  L.mk_part = take(3 * (size_t)num_sms * L.mk_maxj * mk_tile_rows() * 4);
+  L.mk_part = take(3 * (size_t)mk_g * L.mk_maxj * mk_tile_rows() * 4);
   L.mk_apart = take((size_t)num_sms * 8 * 130 * 4);
   L.mk_lm = take((size_t)num_sms * 3 * 4);
   L.mk_prof = take((size_t)SR_PROF_EVENTS * 8);
@@ -192,7 +203,7 @@ struct Model {
       const int N3[3] = {qkv_rows, d.d_model, d.d_model};
       const int K3[3] = {d.d_model, q_dim, d.d_ffn};
       std::vector<uint16_t> tab(3 * 256, 0);
-      const long G = num_sms;
+      const long G = mk_ctas_for(num_sms);
       if (G > 255) return fail(SR_E_INVALID, "decode tables assume <= 255 SMs");
       for (int t = 0; t < 3; ++t) {
         const int tcol = std::min(K3[t], mk_tile_cols());
@@ -229,7 +240,7 @@ struct Model {
     p.v_pool = v_pool;
     p.hA = at<float>(L.mk_h);
     p.hB = p.hA + d.d_model;
-    const size_t pstride = (size_t)num_sms * L.mk_maxj * mk_tile_rows();
+    const size_t pstride = (size_t)mk_ctas_for(num_sms) * L.mk_maxj * mk_tile_rows();
     p.part_qkv = at<float>(L.mk_part);
     p.part_o = p.part_qkv + pstride;
     p.part_d = p.part_o + pstride;
@@ -868,7 +879,7 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
     }
   } else if (!m->stream_decode && !m->graph_decode) {
     // one persistent kernel decodes the whole step (decode_mk.cu)
-    SR_CK(mk_launch(m->mk, m->num_sms, s));
+    SR_CK(mk_launch(m->mk, mk_ctas_for(m->num_sms), s));
   } else if (m->graph_decode) {
     SR_CK(cudaGraphLaunch(m->exec, s));
   } else {
