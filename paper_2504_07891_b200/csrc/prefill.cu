@@ -207,7 +207,33 @@ SR_DEV float sum_splits(const float* part, int splits, size_t stride, size_t idx
   return v;
 }
 
-// q/k: bias + RoPE (pairs j, j+64); k, v -> pages; q -> bf16 buffer
+// 4 consecutive outputs: sum over the splits (same order as sum_splits) + bias
+SR_DEV float4 sum_splits4_bias(const float* part, int splits, size_t stride, size_t idx,
+                               const __nv_bfloat16* bias) {
+  float4 a[8];
+#pragma unroll
+  for (int sp = 0; sp < 8; ++sp)
+    a[sp] = sp < splits ? __ldcg(reinterpret_cast<const float4*>(part + sp * stride + idx))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int sp = 0; sp < 8; ++sp) {
+    t.x += a[sp].x;
+    t.y += a[sp].y;
+    t.z += a[sp].z;
+    t.w += a[sp].w;
+  }
+  const uint2 b = *reinterpret_cast<const uint2*>(bias);
+  const float2 b01 = bf2_to_f2(b.x), b23 = bf2_to_f2(b.y);
+  return make_float4(t.x + b01.x, t.y + b01.y, t.z + b23.x, t.w + b23.y);
+}
+
+SR_DEV void store_bf16x4(__nv_bfloat16* dst, float a, float b, float c, float d) {
+  *reinterpret_cast<uint2*>(dst) = make_uint2(f2_to_bf2(a, b), f2_to_bf2(c, d));
+}
+
+// q/k: bias + RoPE (pairs j, j+64); k, v -> pages; q -> bf16 buffer.
+// A thread takes 4 rotation pairs (or 4 v values): 16-byte partial loads.
 __global__ void epi_qkv_kernel(EpiParams p) {
   grid_launch_dependents();
   grid_wait();
@@ -215,33 +241,37 @@ __global__ void epi_qkv_kernel(EpiParams p) {
   const int pos = p.start_pos + m;
   const size_t stride = (size_t)p.M * p.N;
   const int qk = p.q_dim + p.kv_dim;
-  const int n_pairs = p.N / 2;
+  const int nq4 = qk / 8, nv4 = p.kv_dim / 4;
   const int page = p.page_table[pos / kPage];
-  for (int t = threadIdx.x; t < n_pairs; t += blockDim.x) {
-    int r0, r1;
-    if (t < qk / 2) { r0 = (t / kHalf) * kHeadDim + t % kHalf; r1 = r0 + kHalf; }
-    else { r0 = qk + 2 * (t - qk / 2); r1 = r0 + 1; }
-    const float v0 = sum_splits(p.part, p.splits, stride, (size_t)m * p.N + r0) + bf_to_f(p.bias[r0]);
-    const float v1 = sum_splits(p.part, p.splits, stride, (size_t)m * p.N + r1) + bf_to_f(p.bias[r1]);
-    if (r0 < qk) {
-      const int j = r0 % kHeadDim;
-      const float c = p.rope[((size_t)pos * kHalf + j) * 2];
-      const float s = p.rope[((size_t)pos * kHalf + j) * 2 + 1];
-      const float y0 = v0 * c - v1 * s, y1 = v1 * c + v0 * s;
+  const size_t row = (size_t)m * p.N;
+  for (int t = threadIdx.x; t < nq4 + nv4; t += blockDim.x) {
+    if (t < nq4) {
+      const int j = (t % (kHalf / 4)) * 4;
+      const int r0 = (t / (kHalf / 4)) * kHeadDim + j, r1 = r0 + kHalf;
+      const float4 v0 = sum_splits4_bias(p.part, p.splits, stride, row + r0, p.bias + r0);
+      const float4 v1 = sum_splits4_bias(p.part, p.splits, stride, row + r1, p.bias + r1);
+      const float4* rp = reinterpret_cast<const float4*>(p.rope + ((size_t)pos * kHalf + j) * 2);
+      const float4 cs01 = rp[0], cs23 = rp[1];  // (c, s) of j .. j+3
+      const float y0[4] = {v0.x * cs01.x - v1.x * cs01.y, v0.y * cs01.z - v1.y * cs01.w,
+                           v0.z * cs23.x - v1.z * cs23.y, v0.w * cs23.z - v1.w * cs23.w};
+      const float y1[4] = {v1.x * cs01.x + v0.x * cs01.y, v1.y * cs01.z + v0.y * cs01.w,
+                           v1.z * cs23.x + v0.z * cs23.y, v1.w * cs23.z + v0.w * cs23.w};
+      __nv_bfloat16 *d0, *d1;
       if (r0 < p.q_dim) {
-        p.q[(size_t)m * p.q_dim + r0] = __float2bfloat16_rn(y0);
-        p.q[(size_t)m * p.q_dim + r1] = __float2bfloat16_rn(y1);
+        d0 = p.q + (size_t)m * p.q_dim + r0;
+        d1 = d0 + kHalf;
       } else {
         const int kvh = (r0 - p.q_dim) / kHeadDim;
-        const size_t base = kv_offset(p.layer, page, kvh, pos % kPage, p.n_pages, p.n_kv);
-        p.k_pool[base + j] = __float2bfloat16_rn(y0);
-        p.k_pool[base + j + kHalf] = __float2bfloat16_rn(y1);
+        d0 = p.k_pool + kv_offset(p.layer, page, kvh, pos % kPage, p.n_pages, p.n_kv) + j;
+        d1 = d0 + kHalf;
       }
+      store_bf16x4(d0, y0[0], y0[1], y0[2], y0[3]);
+      store_bf16x4(d1, y1[0], y1[1], y1[2], y1[3]);
     } else {
-      const int vr = r0 - qk, kvh = vr / kHeadDim, dd = vr % kHeadDim;
-      const size_t base = kv_offset(p.layer, page, kvh, pos % kPage, p.n_pages, p.n_kv);
-      p.v_pool[base + dd] = __float2bfloat16_rn(v0);
-      p.v_pool[base + dd + 1] = __float2bfloat16_rn(v1);
+      const int vr = 4 * (t - nq4), kvh = vr / kHeadDim, dd = vr % kHeadDim;
+      const float4 v = sum_splits4_bias(p.part, p.splits, stride, row + qk + vr, p.bias + qk + vr);
+      store_bf16x4(p.v_pool + kv_offset(p.layer, page, kvh, pos % kPage, p.n_pages, p.n_kv) + dd,
+                   v.x, v.y, v.z, v.w);
     }
   }
 }
@@ -250,7 +280,9 @@ cudaError_t epi_qkv_launch(const EpiParams& p, cudaStream_t stream) {
   return launch_pdl(epi_qkv_kernel, dim3(p.M), kEpiRowThreads, 0, stream, p);
 }
 
-// h[m] += sum_s part;  x[m] = bf16(rmsnorm(h[m]) * w)   (N == d)
+// h[m] += sum_s part;  x[m] = bf16(rmsnorm(h[m]) * w)   (N == d, d % 4 == 0)
+// 16-byte loads of h and of every split's partial; same summation order as
+// sum_splits (splits 0..7 in turn, then added to h)
 __global__ void epi_resid_norm_kernel(EpiParams p) {
   grid_launch_dependents();
   grid_wait();
@@ -258,21 +290,50 @@ __global__ void epi_resid_norm_kernel(EpiParams p) {
   __shared__ float red[32];
   const int m = blockIdx.x, d = p.N;
   const size_t stride = (size_t)p.M * p.N;
+  float4* h4 = reinterpret_cast<float4*>(p.h + (size_t)m * d);
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float v = p.h[(size_t)m * d + i] + sum_splits(p.part, p.splits, stride, (size_t)m * d + i);
-    p.h[(size_t)m * d + i] = v;
-    hrow[i] = v;
-    ss += v * v;
+  for (int i = threadIdx.x; i < (d >> 2); i += blockDim.x) {
+    const size_t idx = (size_t)m * d + 4 * (size_t)i;
+    float4 a[8];
+#pragma unroll
+    for (int sp = 0; sp < 8; ++sp)
+      a[sp] = sp < p.splits ? __ldcg(reinterpret_cast<const float4*>(p.part + sp * stride + idx))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int sp = 0; sp < 8; ++sp) {
+      t.x += a[sp].x;
+      t.y += a[sp].y;
+      t.z += a[sp].z;
+      t.w += a[sp].w;
+    }
+    float4 v = h4[i];
+    v.x += t.x;
+    v.y += t.y;
+    v.z += t.z;
+    v.w += t.w;
+    h4[i] = v;
+    reinterpret_cast<float4*>(hrow)[i] = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   ss = block_sum(ss, red);
   const float rstd = rsqrtf(ss / d + p.eps);
-  for (int i = threadIdx.x; i < d; i += blockDim.x)
-    p.x[(size_t)m * d + i] = __float2bfloat16_rn(hrow[i] * rstd * bf_to_f(p.norm_w[i]));
+  const uint2* w4 = reinterpret_cast<const uint2*>(p.norm_w);
+  uint2* x4 = reinterpret_cast<uint2*>(p.x + (size_t)m * d);
+  for (int i = threadIdx.x; i < (d >> 2); i += blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(hrow)[i];
+    const uint2 w = w4[i];
+    const float2 w01 = bf2_to_f2(w.x), w23 = bf2_to_f2(w.y);
+    x4[i] = make_uint2(f2_to_bf2(v.x * rstd * w01.x, v.y * rstd * w01.y),
+                       f2_to_bf2(v.z * rstd * w23.x, v.w * rstd * w23.y));
+  }
 }
 
 cudaError_t epi_resid_norm_launch(const EpiParams& p, cudaStream_t stream) {
-  return launch_pdl(epi_resid_norm_kernel, dim3(p.M), kEpiRowThreads, p.N * sizeof(float), stream, p);
+  // few rows: wide CTAs keep many loads in flight per row; many rows (batched
+  // verify): 256 threads, so that every row is resident in one wave
+  const int threads = p.M >= 256 ? 256 : kEpiRowThreads;
+  return launch_pdl(epi_resid_norm_kernel, dim3(p.M), threads, p.N * sizeof(float), stream, p);
 }
 
 // act[m][u] = bf16(silu(gate) * up) from interleaved 16-row blocks
