@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    const uint32_t idesc = umma_idesc(NT);
+    // a ragged last token tile multiplies only its live columns (N % 16 == 0)
+    const int rem = M - m0;
+    const uint32_t idesc = umma_idesc(rem >= NT ? NT : ((rem + 15) & ~15));
     for (int i = 0; i < nkb; ++i) {
       const int s = i % stages;
       const uint32_t ph = (uint32_t)(i / stages) & 1u;
@@ -132,8 +134,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int row = n0 + warp * 32 + lane;  // weight row == TMEM lane
     float* Cs = C + (size_t)split * M * N;
+    const int n_live = min(NT, M - m0);
 #pragma unroll 1
-    for (int j = 0; j < NT; j += 32) {
+    for (int j = 0; j < n_live; j += 32) {
       uint32_t v[32];
       const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)j;
       asm volatile(
@@ -281,12 +284,14 @@ __global__ void __launch_bounds__(kPsThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer ----------------
-      const uint32_t idesc = umma_idesc(NT);
       int it = 0, j = 0;
       for (int w = blockIdx.x; w < items; w += gridDim.x, ++j) {
         int n0, m0, kb0, nkb;
         item_coords(w, n0, m0, kb0, nkb);
         const int b = j & 1;
+        // a ragged last token tile multiplies only its live columns (N % 16 == 0)
+        const int rem = M - m0;
+        const uint32_t idesc = umma_idesc(rem >= NT ? NT : ((rem + 15) & ~15));
         mbar_wait(&tempty[b], (((uint32_t)j >> 1) & 1u) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + (uint32_t)(b * kAccCols);
@@ -323,8 +328,9 @@ __global__ void __launch_bounds__(kPsThreads, 1)
       const int split = w % splits;
       const int row = n0 + q * 32 + lane;
       float* Cs = C + (size_t)split * M * N;
+      const int n_live = min(NT, M - m0);
 #pragma unroll 1
-      for (int jj = 0; jj < NT; jj += 32) {
+      for (int jj = 0; jj < n_live; jj += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * kAccCols + jj);
         asm volatile(
