@@ -253,8 +253,10 @@ __global__ void __launch_bounds__(kPsThreads, 1)
   auto item_coords = [&](int w, int& n0, int& m0, int& kb0, int& nkb) {
     const int sp = w % splits;
     const int t = w / splits;
-    n0 = (t % n_tiles_n) * kWRows;
-    m0 = (t / n_tiles_n) * NT;
+    // token tiles fastest: the CTAs running at the same time share weight
+    // tiles, so each weight tile is read from HBM once (not once per token tile)
+    m0 = (t % n_tiles_m) * NT;
+    n0 = (t / n_tiles_m) * kWRows;
     kb0 = sp * per;
     const int kb1 = min(nkb_total, kb0 + per);
     nkb = kb1 > kb0 ? kb1 - kb0 : 0;
