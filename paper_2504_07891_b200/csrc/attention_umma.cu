@@ -386,9 +386,14 @@ __global__ void __launch_bounds__(kFaThreads, 2)
 
 int attn_umma_splits(int n_kv, int q_tiles, int T, int num_sms) {
   const int tiles = (T + kPage - 1) / kPage;
+  static const int cap = [] {  // tuning knob: most KV splits per query tile
+    const char* e = getenv("SR_ATTN_SPLITS_MAX");
+    const int v = e ? atoi(e) : 8;  // 8 vs 16: 4.37 vs 4.48 ms (7B, M = 80, 2 K context)
+    return v < 1 ? 1 : v > 16 ? 16 : v;
+  }();
   int s = 2 * num_sms / (n_kv * q_tiles);  // two CTAs per SM
   if (s > tiles) s = tiles;
-  if (s > 16) s = 16;
+  if (s > cap) s = cap;
   return s < 1 ? 1 : s;
 }
 
