@@ -244,7 +244,7 @@ __global__ void epi_qkv_kernel(EpiParams p) {
   const int nq4 = qk / 8, nv4 = p.kv_dim / 4;
   const int page = p.page_table[pos / kPage];
   const size_t row = (size_t)m * p.N;
-  for (int t = threadIdx.x; t < nq4 + nv4; t += blockDim.x) {
+  for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < nq4 + nv4; t += gridDim.y * blockDim.x) {
     if (t < nq4) {
       const int j = (t % (kHalf / 4)) * 4;
       const int r0 = (t / (kHalf / 4)) * kHeadDim + j, r1 = r0 + kHalf;
@@ -277,7 +277,10 @@ __global__ void epi_qkv_kernel(EpiParams p) {
 }
 
 cudaError_t epi_qkv_launch(const EpiParams& p, cudaStream_t stream) {
-  return launch_pdl(epi_qkv_kernel, dim3(p.M), kEpiRowThreads, 0, stream, p);
+  // a row's (4-pair / 4-value) groups spread over 256-thread CTAs: short verify
+  // passes still put several CTAs per row in flight
+  const int groups = (p.q_dim + p.kv_dim) / 8 + p.kv_dim / 4;
+  return launch_pdl(epi_qkv_kernel, dim3(p.M, (groups + 255) / 256), 256, 0, stream, p);
 }
 
 // h[m] += sum_s part;  x[m] = bf16(rmsnorm(h[m]) * w)   (N == d, d % 4 == 0)
