@@ -171,6 +171,29 @@ int sr_verify_tokens(void* model, const int32_t* page_table, int32_t start_pos,
                      void* stream);
 
 /*
+ * Multi-sequence passes (several trajectories per GPU).  n_seq
+ * streams (n_seq <= 64) each feed n_ids[i] fresh tokens at positions
+ * start_pos[i].. of their own page table page_tables[i] (host array of device
+ * pointers; start_pos, n_ids: host arrays).  ids (device) holds the
+ * sequences' tokens back to back, sum(n_ids) <= max_tokens; tok_meta (device,
+ * int32 pairs) holds (position, page id) of every row.  One weight stream
+ * serves all rows; attention runs per sequence.
+ *
+ * sr_score_batch: the judge readout of sr_score at each sequence's last row,
+ *   readouts[i] (device).
+ * sr_step_batch: the greedy choice at each sequence's last row, out_ids[i]
+ *   (ties: lower id) and margins[i] (may be NULL) -- one batched decode step
+ *   when every n_ids[i] == 1, the first token after a prompt otherwise.
+ */
+int sr_score_batch(void* model, int32_t n_seq, const int32_t* const* page_tables,
+                   const int32_t* start_pos, const int32_t* n_ids, const int32_t* ids,
+                   const int32_t* tok_meta, const int8_t* first_digit, int32_t threshold,
+                   sr_readout* readouts, void* stream);
+int sr_step_batch(void* model, int32_t n_seq, const int32_t* const* page_tables,
+                  const int32_t* start_pos, const int32_t* n_ids, const int32_t* ids,
+                  const int32_t* tok_meta, int32_t* out_ids, float* margins, void* stream);
+
+/*
  * Test hook: prefill ids and write fp32 logits of every new position
  * (`all` != 0, logits [n_ids, vocab_rows]) or of the last one ([vocab_rows]).
  */

@@ -93,6 +93,13 @@ class RefEngine:
         out = [argmax_margin(masked(row, self.vocab.n_text)) for row in logits]
         return [t for t, _ in out], [m for _, m in out]
 
+    # multi-sequence calls: the oracle answers them one sequence at a time
+    def score_batch(self, streams, suffixes, threshold: int) -> list[Readout]:
+        return [self.score(s, suf, threshold) for s, suf in zip(streams, suffixes)]
+
+    def generate_batch(self, streams, suffixes, max_new: int, stop: tuple[str, ...]):
+        return [self.generate(s, suf, max_new, stop) for s, suf in zip(streams, suffixes)]
+
     def logits_teacher_forced(self, ids: Sequence[int]) -> torch.Tensor:
         """[n, V] logits of every position of ``ids`` from an empty cache."""
         cache = self.model.new_cache()

@@ -28,7 +28,7 @@ from .domain import BackendProfile, BackendRole
 from .host import ModelBackend, Readout, Stream
 from .shapes import (PAIRS, ModelSpec, get_spec, make_tp_weights, make_weights, rope_table,
                      shard_weights, tensor_shapes, tp_spec)
-from .vocab import Vocab, shared_vocab
+from .vocab import CLASS_END_THINK, CLASS_STOP, Vocab, shared_vocab
 
 PAGE = native.SR_PAGE
 
@@ -92,6 +92,7 @@ class DeviceModel:
                 C.byref(self.desc), C.byref(ptrs), C.c_void_p(stream), C.byref(handle)))
         self.handle = handle
         self.free_pages = list(range(n_pages - 1, -1, -1))
+        self.max_tokens = max_tokens
         # staging
         self.ids_host = torch.empty(max_pos, dtype=torch.int32, pin_memory=True)
         self.ids_dev = torch.empty(max_pos, dtype=torch.int32, device=self.device)
@@ -219,7 +220,7 @@ class NativeEngine:
             self.model.free_pages.append(pg.pages.pop())
         pg.synced = min(pg.synced, len(pg.pages))
 
-    def _ensure(self, stream: Stream, n_positions: int) -> None:
+    def _ensure(self, stream: Stream, n_positions: int, protect=()) -> None:
         if n_positions > self.model.max_pos:
             raise ValueError(f"context of {n_positions} positions exceeds max_pos "
                              f"{self.model.max_pos}")
@@ -228,7 +229,8 @@ class NativeEngine:
         free = self.model.free_pages
         while len(pg.pages) < need:
             if not free:
-                victims = sorted((s for s in self.streams if s is not stream and s.handle.pages),
+                victims = sorted((s for s in self.streams
+                                  if s is not stream and s not in protect and s.handle.pages),
                                  key=lambda s: s.stamp)
                 if not victims:
                     raise MemoryError("K/V page pool exhausted")
@@ -291,6 +293,127 @@ class NativeEngine:
         margin = r[2:3].view(torch.float32).item()
         return Readout(score=int(r[0]), accept=bool(int(r[1])), flags=0, margin=margin,
                        argmax=int(r[3]))
+
+    # -- multi-sequence passes ----------------------------
+    def _batch(self, streams: Sequence[Stream], suffixes: Sequence[Sequence[int]],
+               room: int = 0):
+        """Stage one multi-sequence pass: pages for every stream (no stream of
+        the batch is evicted for another), the ids back to back, and the
+        (position, page) of every row."""
+        m = self.model
+        if len(set(id(s) for s in streams)) != len(streams):
+            raise ValueError("a batched pass needs distinct streams")
+        starts, counts, meta, flat = [], [], [], []
+        for st, suf in zip(streams, suffixes):
+            start = len(st.ids)
+            self._ensure(st, start + len(suf) + room, protect=streams)
+            pages = st.handle.pages
+            for i in range(len(suf)):
+                meta += [start + i, pages[(start + i) // PAGE]]
+            starts.append(start)
+            counts.append(len(suf))
+            flat.extend(suf)
+        n = len(streams)
+        ids_ptr = m.upload_ids(flat)
+        meta_t = torch.as_tensor(meta, dtype=torch.int32).pin_memory()
+        meta_dev = meta_t.to(m.device, non_blocking=True)
+        tables = (C.c_void_p * n)(*[st.handle.table_dev.data_ptr() for st in streams])
+        return (n, tables, (C.c_int32 * n)(*starts), (C.c_int32 * n)(*counts),
+                C.c_void_p(ids_ptr), meta_dev, len(flat))
+
+    def _passes(self, lengths: Sequence[int]) -> list[list[int]]:
+        """Group sequences (in order) into passes of at most max_tokens rows."""
+        cap = self.model.max_tokens
+        out, cur, rows = [], [], 0
+        for i, n in enumerate(lengths):
+            if cur and rows + n > cap:
+                out.append(cur)
+                cur, rows = [], 0
+            cur.append(i)
+            rows += n
+        if cur:
+            out.append(cur)
+        return out
+
+    def score_batch(self, streams: Sequence[Stream], suffixes: Sequence[Sequence[int]],
+                    threshold: int) -> list[Readout]:
+        """``score`` for several streams, as few passes (``sr_score_batch``)
+        as max_tokens rows allow; a sequence longer than that alone takes the
+        chunked single-sequence path."""
+        res: list[Readout | None] = [None] * len(streams)
+        for group in self._passes([len(s) for s in suffixes]):
+            if len(group) == 1 and len(suffixes[group[0]]) > self.model.max_tokens:
+                i = group[0]
+                res[i] = self.score(streams[i], suffixes[i], threshold)
+                continue
+            sub = self._score_pass([streams[i] for i in group], [suffixes[i] for i in group],
+                                   threshold)
+            for i, r in zip(group, sub):
+                res[i] = r
+        return res
+
+    def _score_pass(self, streams, suffixes, threshold: int) -> list[Readout]:
+        m = self.model
+        n, tables, starts, counts, ids, meta_dev, rows = self._batch(streams, suffixes)
+        out = torch.zeros(4 * n, dtype=torch.int32, device=m.device)
+        native.check("sr_score_batch", m.lib.sr_score_batch(
+            m.handle, n, tables, starts, counts, ids, C.c_void_p(meta_dev.data_ptr()),
+            C.c_void_p(self.first_digit.data_ptr()), int(threshold), C.c_void_p(out.data_ptr()),
+            m.stream_ptr))
+        host = out.cpu()
+        self.stats.calls += 1
+        self.stats.prefill_ms += m.timing().prefill_ms
+        self.stats.prefill_tokens += rows
+        res = []
+        for i, (st, suf) in enumerate(zip(streams, suffixes)):
+            st.ids.extend(suf)
+            r = host[4 * i:4 * i + 4]
+            res.append(Readout(score=int(r[0]), accept=bool(int(r[1])), flags=0,
+                               margin=r[2:3].view(torch.float32).item(), argmax=int(r[3])))
+        return res
+
+    def generate_batch(self, streams: Sequence[Stream], suffixes: Sequence[Sequence[int]],
+                       max_new: int, stop: tuple[str, ...]) -> list[tuple[list[int], int]]:
+        """Greedy ``generate`` for several streams, one batched step per token
+        (``sr_step_batch``): each step streams the weights once for every live
+        sequence.  Finished sequences leave the batch."""
+        from .host import finish_of
+
+        m = self.model
+        classes = self.vocab.token_classes(stop, self.n_ids)
+        live = list(range(len(streams)))
+        gens: list[list[int]] = [[] for _ in streams]
+        feed = [list(s) for s in suffixes]
+        out = torch.zeros(len(streams), dtype=torch.int32, device=m.device)
+        margins = torch.zeros(len(streams), dtype=torch.float32, device=m.device)
+        self.last_margins = []
+        for i in live:  # prompts beyond one pass: all but the last token on the chunked path
+            if len(feed[i]) > m.max_tokens:
+                self.prefill(streams[i], feed[i][:-1])
+                feed[i] = feed[i][-1:]
+        while live:
+            toks = []
+            for group in self._passes([len(feed[i]) for i in live]):
+                idx = [live[g] for g in group]
+                n, tables, starts, counts, ids, meta_dev, rows = self._batch(
+                    [streams[i] for i in idx], [feed[i] for i in idx], room=max_new)
+                native.check("sr_step_batch", m.lib.sr_step_batch(
+                    m.handle, n, tables, starts, counts, ids, C.c_void_p(meta_dev.data_ptr()),
+                    C.c_void_p(out.data_ptr()), C.c_void_p(margins.data_ptr()), m.stream_ptr))
+                toks += out[:n].tolist()
+                self.stats.calls += 1
+                self.stats.prefill_ms += m.timing().prefill_ms
+                self.stats.prefill_tokens += rows
+            nxt = []
+            for k, i in enumerate(live):
+                streams[i].ids.extend(feed[i])
+                gens[i].append(toks[k])
+                if classes[toks[k]] in (CLASS_STOP, CLASS_END_THINK) or len(gens[i]) >= max_new:
+                    continue
+                feed[i] = [toks[k]]
+                nxt.append(i)
+            live = nxt
+        return [(g, finish_of(g, classes)) for g in gens]
 
     def prefill(self, stream: Stream, suffix: Sequence[int]) -> None:
         """Commit ``suffix`` to the stream's K/V (no token is chosen)."""

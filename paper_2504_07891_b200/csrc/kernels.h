@@ -159,6 +159,8 @@ struct EpiParams {
   __nv_bfloat16* v_pool;
   const int* page_table;
   int start_pos, layer, n_pages, n_kv, q_dim, kv_dim;
+  const int* tok_meta;  // multi-sequence passes: (position, page) per row; null:
+                        // one sequence, position start_pos + row, page_table
   // glu
   __nv_bfloat16* act;  // [M, f]
 };

@@ -238,11 +238,11 @@ __global__ void epi_qkv_kernel(EpiParams p) {
   grid_launch_dependents();
   grid_wait();
   const int m = blockIdx.x;
-  const int pos = p.start_pos + m;
+  const int pos = p.tok_meta ? p.tok_meta[2 * m] : p.start_pos + m;
   const size_t stride = (size_t)p.M * p.N;
   const int qk = p.q_dim + p.kv_dim;
   const int nq4 = qk / 8, nv4 = p.kv_dim / 4;
-  const int page = p.page_table[pos / kPage];
+  const int page = p.tok_meta ? p.tok_meta[2 * m + 1] : p.page_table[pos / kPage];
   const size_t row = (size_t)m * p.N;
   for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < nq4 + nv4; t += gridDim.y * blockDim.x) {
     if (t < nq4) {

@@ -420,6 +420,13 @@ struct Model {
   }
 
   // ------------------------------------------------------------ prefill ---
+  // One sequence's rows inside a prefill pass: rows [row0, row0 + M) sit at
+  // positions start.. of the stream whose page table is `page_table`.
+  struct SeqSpan {
+    const int* page_table;
+    int start, row0, M;
+  };
+
   // Runs ids[0..n) at positions start.. through all layers, chunked by
   // max_tokens; leaves the final-normed rows of the last chunk in x.
   // Returns the row count of the last chunk.
@@ -429,84 +436,99 @@ struct Model {
     int rows = 0;
     for (int c0 = 0; c0 < n; c0 += T) {
       const int M = std::min(T, n - c0);
-      const int pos0 = start + c0;
       rows = M;
-      SR_CK(embed_norm_launch(ids + c0, M, embed, d.d_model, lw(0, LN1), d.rms_eps, h, x, s));
-      for (int l = 0; l < d.n_layers; ++l) {
-        // qkv
-        int rc = gemm(ACT_X, l * 4 + 0, x, lw(l, WQKV), M, qkv_rows, d.d_model, s);
-        if (rc) return -rc;
-        EpiParams ep = epi_base(M, qkv_rows);
-        ep.bias = lw(l, BQKV);
-        ep.q = q;
-        ep.page_table = page_table;
-        ep.start_pos = pos0;
-        ep.layer = l;
-        SR_CK(epi_qkv_launch(ep, s));
-        watch(s, "qkv gemm+epi", l, M, last_splits);
-        // attention
+      const SeqSpan sp{page_table, start + c0, 0, M};
+      if (int rc = run_layers(ids + c0, M, &sp, 1, nullptr, s)) return rc;
+    }
+    *last_rows = rows;
+    return 0;
+  }
+
+  // One pass of M rows (<= max_tokens) through every layer.  The rows may
+  // belong to several sequences (spans): the GEMMs and epilogues run over all
+  // rows at once, attention runs per span over that span's own K/V pages.
+  // tok_meta (device, (position, page) per row) is required when n_spans > 1.
+  int run_layers(const int* ids, int M, const SeqSpan* spans, int n_spans, const int* tok_meta,
+                 cudaStream_t s) {
+    SR_CK(embed_norm_launch(ids, M, embed, d.d_model, lw(0, LN1), d.rms_eps, h, x, s));
+    for (int l = 0; l < d.n_layers; ++l) {
+      // qkv
+      int rc = gemm(ACT_X, l * 4 + 0, x, lw(l, WQKV), M, qkv_rows, d.d_model, s);
+      if (rc) return -rc;
+      EpiParams ep = epi_base(M, qkv_rows);
+      ep.bias = lw(l, BQKV);
+      ep.q = q;
+      ep.page_table = spans[0].page_table;
+      ep.start_pos = spans[0].start;
+      ep.tok_meta = tok_meta;
+      ep.layer = l;
+      SR_CK(epi_qkv_launch(ep, s));
+      watch(s, "qkv gemm+epi", l, M, last_splits);
+      // attention, per sequence
+      for (int k = 0; k < n_spans; ++k) {
+        const SeqSpan& sp = spans[k];
         AttnParams a{};
-        a.q = q;
-        a.out = attn;
+        a.q = q + (size_t)sp.row0 * q_dim;
+        a.out = attn + (size_t)sp.row0 * q_dim;
         a.k_pool = k_pool;
         a.v_pool = v_pool;
-        a.page_table = page_table;
+        a.page_table = sp.page_table;
         a.part = apart;
         a.counters = actr;
         a.layer = l;
         a.n_pages = d.n_pages;
         a.n_heads = d.n_heads;
         a.n_kv = d.n_kv_heads;
-        const int Tlast = pos0 + M;
-        a.start_pos = pos0;
+        const int Tlast = sp.start + sp.M;
+        a.start_pos = sp.start;
         a.st = nullptr;
         if (attn_simt) {
           a.nsplit = std::min(kAttnPrefillSplit, attn_prefill_splits(Tlast));
-          SR_CK(attn_prefill_launch(a, M, s));
+          SR_CK(attn_prefill_launch(a, sp.M, s));
         } else if (attn_umma) {
           const int G = d.n_heads / d.n_kv_heads;
-          a.nsplit = std::min(kAttnPrefillSplit,
-                              attn_umma_splits(d.n_kv_heads, attn_umma_q_tiles(M, G), Tlast, num_sms));
-          SR_CK(attn_umma_launch(&kvmaps[0].m, &kvmaps[1].m, a, M, a.nsplit, s));
-          if (a.nsplit > 1) SR_CK(attn_merge_launch(a, M, a.nsplit, s));
-          watch(s, "attn_prefill_umma", l, M, a.nsplit);
+          a.nsplit = std::min(kAttnPrefillSplit, attn_umma_splits(d.n_kv_heads,
+                                                                  attn_umma_q_tiles(sp.M, G),
+                                                                  Tlast, num_sms));
+          SR_CK(attn_umma_launch(&kvmaps[0].m, &kvmaps[1].m, a, sp.M, a.nsplit, s));
+          if (a.nsplit > 1) SR_CK(attn_merge_launch(a, sp.M, a.nsplit, s));
+          watch(s, "attn_prefill_umma", l, sp.M, a.nsplit);
         } else {
           const int G = d.n_heads / d.n_kv_heads;
-          const int q_tiles = (M * G + 63) / 64;
+          const int q_tiles = (sp.M * G + 63) / 64;
           a.nsplit = std::min(kAttnPrefillSplit, attn_tc_splits(d.n_kv_heads, q_tiles, Tlast, num_sms));
           a.sep_merge = 1;
           a.p_hi_only = p_hi_only ? 1 : 0;
-          SR_CK(attn_tc_launch(a, M, a.nsplit, s, true));
-          if (a.nsplit > 1) SR_CK(attn_merge_launch(a, M, a.nsplit, s));
-          watch(s, "attn_prefill_tc", l, M, a.nsplit);
+          SR_CK(attn_tc_launch(a, sp.M, a.nsplit, s, true));
+          if (a.nsplit > 1) SR_CK(attn_merge_launch(a, sp.M, a.nsplit, s));
+          watch(s, "attn_prefill_tc", l, sp.M, a.nsplit);
         }
-        // o-proj + residual + norm2
-        rc = gemm(ACT_ATTN, l * 4 + 1, attn, lw(l, WO), M, d.d_model, q_dim, s);
-        if (rc) return -rc;
-        ep = epi_base(M, d.d_model);
-        ep.norm_w = lw(l, LN2);
-        if (tp_comm)
-          if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
-        SR_CK(epi_resid_norm_launch(ep, s));
-        // gate/up
-        rc = gemm(ACT_X, l * 4 + 2, x, lw(l, WGU), M, 2 * d.d_ffn, d.d_model, s, act);
-        if (rc) return -rc;
-        if (!fused_glu) {
-          ep = epi_base(M, 2 * d.d_ffn);
-          SR_CK(epi_glu_launch(ep, s));
-        }
-        watch(s, "o/gu gemm+epi", l, M, last_splits);
-        // down + residual + next norm
-        rc = gemm(ACT_ACT, l * 4 + 3, act, lw(l, WD), M, d.d_model, d.d_ffn, s);
-        if (rc) return -rc;
-        ep = epi_base(M, d.d_model);
-        ep.norm_w = (l + 1 < d.n_layers) ? lw(l + 1, LN1) : ln_f;
-        if (tp_comm)
-          if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
-        SR_CK(epi_resid_norm_launch(ep, s));
       }
+      // o-proj + residual + norm2
+      rc = gemm(ACT_ATTN, l * 4 + 1, attn, lw(l, WO), M, d.d_model, q_dim, s);
+      if (rc) return -rc;
+      ep = epi_base(M, d.d_model);
+      ep.norm_w = lw(l, LN2);
+      if (tp_comm)
+        if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
+      SR_CK(epi_resid_norm_launch(ep, s));
+      // gate/up
+      rc = gemm(ACT_X, l * 4 + 2, x, lw(l, WGU), M, 2 * d.d_ffn, d.d_model, s, act);
+      if (rc) return -rc;
+      if (!fused_glu) {
+        ep = epi_base(M, 2 * d.d_ffn);
+        SR_CK(epi_glu_launch(ep, s));
+      }
+      watch(s, "o/gu gemm+epi", l, M, last_splits);
+      // down + residual + next norm
+      rc = gemm(ACT_ACT, l * 4 + 3, act, lw(l, WD), M, d.d_model, d.d_ffn, s);
+      if (rc) return -rc;
+      ep = epi_base(M, d.d_model);
+      ep.norm_w = (l + 1 < d.n_layers) ? lw(l + 1, LN1) : ln_f;
+      if (tp_comm)
+        if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
+      SR_CK(epi_resid_norm_launch(ep, s));
     }
-    *last_rows = rows;
     return 0;
   }
 
@@ -1025,6 +1047,113 @@ int sr_verify_tokens(void* model, const int32_t* page_table, int32_t start_pos,
   SR_CK(cudaEventRecord(m->ev[1], s));
   SR_CK(cudaEventRecord(m->ev[2], s));
   m->timing.prefill_tokens = n_ids;
+  m->timing.decode_tokens = 0;
+  return 0;
+}
+
+// ------------------------------------------------------ multi-sequence ---
+// Several streams' fresh rows in one pass: the GEMMs and
+// epilogues run over all rows at once (one weight stream for the batch),
+// attention runs per sequence, the LM head is one GEMM over each sequence's
+// last row.
+static constexpr int kMaxSeqs = 64;
+
+static int batch_spans(Model* m, int32_t n_seq, const int32_t* const* page_tables,
+                       const int32_t* start_pos, const int32_t* n_ids,
+                       std::vector<Model::SeqSpan>& spans, int* total) {
+  if (n_seq < 1 || n_seq > kMaxSeqs) return fail(SR_E_INVALID, "n_seq out of range");
+  if (!page_tables || !start_pos || !n_ids) return fail(SR_E_INVALID, "null argument");
+  if (m->tp_comm || m->d.tp_world > 1)
+    return fail(SR_E_INVALID, "batched calls: tensor parallelism not supported");
+  spans.resize(n_seq);
+  int row = 0;
+  for (int i = 0; i < n_seq; ++i) {
+    if (!page_tables[i] || n_ids[i] < 1 || start_pos[i] < 0) return fail(SR_E_INVALID, "bad sequence");
+    if (start_pos[i] + n_ids[i] > m->d.max_pos) return fail(SR_E_CAPACITY, "positions exceed max_pos");
+    spans[i] = Model::SeqSpan{page_tables[i], start_pos[i], row, n_ids[i]};
+    row += n_ids[i];
+  }
+  if (row > m->d.max_tokens) return fail(SR_E_CAPACITY, "batched rows exceed max_tokens");
+  *total = row;
+  return 0;
+}
+
+// run the pass, then the LM head over each sequence's last row (gathered into
+// x rows 0..n_seq-1): fp32 logit partials in m->part [splits][n_seq][V]
+static int batch_forward_last(Model* m, const std::vector<Model::SeqSpan>& spans, int M,
+                              const int32_t* ids, const int32_t* tok_meta, cudaStream_t s) {
+  const int n_seq = (int)spans.size();
+  if ((size_t)n_seq * m->d.vocab_rows > m->L.part_floats)
+    return fail(SR_E_CAPACITY, "LM-head partials exceed the workspace");
+  if (int rc = m->run_layers(ids, M, spans.data(), n_seq, tok_meta, s)) return -rc;
+  const size_t row_bytes = (size_t)m->d.d_model * sizeof(__nv_bfloat16);
+  for (int i = 0; i < n_seq; ++i) {  // rows only move down: no copy overwrites a later source
+    const int src = spans[i].row0 + spans[i].M - 1;
+    if (src != i)
+      SR_CK(cudaMemcpyAsync(m->x + (size_t)i * m->d.d_model, m->x + (size_t)src * m->d.d_model,
+                            row_bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  const int rc = m->gemm(Model::ACT_X, m->d.n_layers * 4, m->x, m->lm_head, n_seq,
+                         m->d.vocab_rows, m->d.d_model, s);
+  return rc ? -rc : 0;
+}
+
+int sr_score_batch(void* model, int32_t n_seq, const int32_t* const* page_tables,
+                   const int32_t* start_pos, const int32_t* n_ids, const int32_t* ids,
+                   const int32_t* tok_meta, const int8_t* first_digit, int32_t threshold,
+                   sr_readout* readouts, void* stream) {
+  Model* m = (Model*)model;
+  if (!m || !ids || !tok_meta || !first_digit || !readouts) return fail(SR_E_INVALID, "null argument");
+  std::vector<Model::SeqSpan> spans;
+  int M = 0;
+  if (int rc = batch_spans(m, n_seq, page_tables, start_pos, n_ids, spans, &M)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  SR_CK(cudaEventRecord(m->ev[0], s));
+  if (int rc = batch_forward_last(m, spans, M, ids, tok_meta, s)) return rc;
+  const size_t V = m->d.vocab_rows;
+  for (int i = 0; i < n_seq; ++i) {
+    ReadoutParams r{};
+    if (m->last_splits == 1) {
+      r.logits = m->part + (size_t)i * V;
+    } else {
+      SR_CK(split_sum_launch(m->part + (size_t)i * V, m->last_splits, (size_t)n_seq * V, m->logits,
+                             V, s));
+      r.logits = m->logits;
+    }
+    r.n_valid = m->d.vocab_text;
+    r.first_digit = first_digit;
+    r.threshold = threshold;
+    r.counts = m->ro_cnt;
+    r.part_v1 = m->lm_v1;
+    r.part_v2 = m->lm_v2;
+    r.part_i1 = m->lm_i1;
+    r.out = readouts + i;
+    SR_CK(readout_launch(r, m->num_sms, s));
+  }
+  SR_CK(cudaEventRecord(m->ev[1], s));
+  SR_CK(cudaEventRecord(m->ev[2], s));
+  m->timing.prefill_tokens = M;
+  m->timing.decode_tokens = 0;
+  return 0;
+}
+
+int sr_step_batch(void* model, int32_t n_seq, const int32_t* const* page_tables,
+                  const int32_t* start_pos, const int32_t* n_ids, const int32_t* ids,
+                  const int32_t* tok_meta, int32_t* out_ids, float* margins, void* stream) {
+  Model* m = (Model*)model;
+  if (!m || !ids || !tok_meta || !out_ids) return fail(SR_E_INVALID, "null argument");
+  std::vector<Model::SeqSpan> spans;
+  int M = 0;
+  if (int rc = batch_spans(m, n_seq, page_tables, start_pos, n_ids, spans, &M)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  SR_CK(cudaEventRecord(m->ev[0], s));
+  if (int rc = batch_forward_last(m, spans, M, ids, tok_meta, s)) return rc;
+  const size_t V = m->d.vocab_rows;
+  SR_CK(rows_argmax_launch(m->part, m->last_splits, (size_t)n_seq * V, n_seq, (int)V,
+                           m->d.vocab_text, m->d.vocab_base, out_ids, margins, s));
+  SR_CK(cudaEventRecord(m->ev[1], s));
+  SR_CK(cudaEventRecord(m->ev[2], s));
+  m->timing.prefill_tokens = M;
   m->timing.decode_tokens = 0;
   return 0;
 }

@@ -118,14 +118,16 @@ class StreamPool:
         self.streams = [Stream(i) for i in range(n)]
         self._clock = 0
 
-    def acquire(self, ids: Sequence[int]) -> tuple[Stream, int]:
+    def acquire(self, ids: Sequence[int], exclude=()) -> tuple[Stream, int]:
         best, best_len = None, -1
         for s in self.streams:
+            if s in exclude:
+                continue
             l = common_prefix(s.ids, ids)
             if l > best_len or (l == best_len and best is not None and s.stamp > best.stamp):
                 best, best_len = s, l
         if best_len == 0:
-            best = min(self.streams, key=lambda s: s.stamp)
+            best = min((s for s in self.streams if s not in exclude), key=lambda s: s.stamp)
         self._clock += 1
         best.stamp = self._clock
         # at least one prompt token is always recomputed: its logits seed decode
@@ -290,6 +292,66 @@ class ModelBackend(Backend):
             if type(exc).__name__ != "NativeError":
                 raise
             raise self._device_error(exc) from exc
+
+    # -- several requests in one device pass -----------------
+    def _acquire_many(self, id_lists):
+        if len(id_lists) > len(self.pool.streams):
+            raise ValueError(f"{len(id_lists)} requests need as many KV streams "
+                             f"(this backend has {len(self.pool.streams)})")
+        chosen, keeps = [], []
+        for ids in id_lists:
+            st, keep = self.pool.acquire(ids, exclude=chosen)
+            self.engine.truncate(st, keep)
+            chosen.append(st)
+            keeps.append(keep)
+        return chosen, keeps
+
+    def score_steps(self, requests: Sequence[VerificationRequest]) -> list:
+        """``score_step`` for several independent requests in one device pass
+        (the engine's ``score_batch``).  Results come back in request order: a
+        ``UtilityScore``, or the ``ScoreParseFailure`` that ``score_step`` would
+        have raised for that request."""
+        T = self.types
+        if self.profile.role != T.BackendRole.BASE:
+            raise ValueError(f"backend {self.profile.name} cannot score steps")
+        render = (domain.render_verification_prompt_v2 if self.verify_template == "v2"
+                  else T.render_verification_prompt)
+        with self._lock:
+            id_lists = [self._prompts.encode(render(r.problem, r.cot_prefix, r.candidate_step))
+                        for r in requests]
+            streams, keeps = self._acquire_many(id_lists)
+            rs = self.engine.score_batch(streams, [ids[k:] for ids, k in zip(id_lists, keeps)],
+                                         self.threshold)
+        return [T.UtilityScore(r.score) if r.score >= 0 else
+                T.ScoreParseFailure("no digit in the top-10 or the sampled token") for r in rs]
+
+    def generate_steps(self, requests: Sequence[GenerationRequest]) -> list:
+        """``generate_step`` for several independent requests, decoded together
+        (the engine's ``generate_batch``: one weight stream per token for all
+        live requests).  Returns ``GenerationResult`` in request order."""
+        T = self.types
+        stops = {tuple(r.stop) for r in requests}
+        if len(stops) != 1 or len({r.max_tokens for r in requests}) != 1:
+            raise ValueError("a batched generation needs one stop list and one max_tokens")
+        t0 = time.monotonic()
+        with self._lock:
+            id_lists = [self._prompts.encode(r.prompt) for r in requests]
+            streams, keeps = self._acquire_many(id_lists)
+            max_new = requests[0].max_tokens
+            outs = self.engine.generate_batch(streams, [ids[k:] for ids, k in zip(id_lists, keeps)],
+                                              max_new, stops.pop())
+        res = []
+        for gen, finish in outs:
+            if finish == FINISH_END_THINK:
+                text_ids, reason = gen[:-1], T.FinishReason.END_THINK
+            elif finish == FINISH_STOP:
+                text_ids, reason = gen, T.FinishReason.STOP
+            else:
+                text_ids, reason = gen, T.FinishReason.LENGTH
+            res.append(T.GenerationResult(text=self.vocab.render(text_ids),
+                                          token_count=len(text_ids), finish_reason=reason,
+                                          measured_latency_s=time.monotonic() - t0))
+        return res
 
     def _generate_step(self, request: GenerationRequest):
         if not request.prompt:

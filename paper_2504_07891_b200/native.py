@@ -59,6 +59,11 @@ EXPORTS = {
     "sr_last_timing": (C.c_int, [C.c_void_p, C.POINTER(Timing)]),
     "sr_verify_tokens": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                    C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sr_score_batch": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                 C.c_void_p]),
+    "sr_step_batch": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sr_debug_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "sr_debug_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "sr_tp_unique_id": (C.c_int, [C.c_void_p]),
