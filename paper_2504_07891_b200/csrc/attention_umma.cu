@@ -117,7 +117,20 @@ __global__ void __launch_bounds__(kFaThreads, 2)
   __shared__ uint32_t tmem_s;
   __shared__ float xch[2][2][kFaRows];  // [page parity][half][row]: row max / sum exchange
 
-  const int g = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
+  const int g = blockIdx.x, split = blockIdx.y;
+  // the sequence (span) and query tile of this CTA: one span (rows 0..M_rows)
+  // unless p.spans lists (first token, tokens, start position, tile) per z
+  int tok0 = 0, span_rows = M_rows, start = p.start_pos, qt = blockIdx.z;
+  const int* ptab = p.page_table;
+  if (p.spans) {
+    const int4 it = p.spans[blockIdx.z];
+    tok0 = it.x;
+    span_rows = it.y * G;
+    start = it.z;
+    qt = it.w;
+    ptab = p.span_tables[blockIdx.z];
+  }
+  const int grow0 = tok0 * G;  // first global query row of the span
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool ctrl = warp == kFaSoftmaxWarps;  // TMA + MMA issue warp
   const int r = tid & (kFaRows - 1);          // query row = TMEM lane
@@ -127,9 +140,8 @@ __global__ void __launch_bounds__(kFaThreads, 2)
   uint8_t* sQ = base;
   uint8_t* sKV = sQ + kFaQBytes;
 
-  const int row0 = qt * kFaRows;
-  const int rows_here = min(kFaRows, M_rows - row0);
-  const int start = p.start_pos;
+  const int row0 = qt * kFaRows;  // within the span
+  const int rows_here = min(kFaRows, span_rows - row0);
   const int last_tok = (row0 + rows_here - 1) / G;
   const int T = start + last_tok + 1;
   const int n_tiles = (T + kPage - 1) / kPage;
@@ -166,7 +178,7 @@ __global__ void __launch_bounds__(kFaThreads, 2)
   if (!ctrl) {
     uint4 v[8];
     if (r < rows_here) {
-      const int rr = row0 + r, tok = rr / G, j = rr % G;
+      const int rr = row0 + r, tok = tok0 + rr / G, j = rr % G;
       const uint4* src = reinterpret_cast<const uint4*>(
           p.q + (size_t)tok * p.n_heads * kHeadDim + (size_t)(g * G + j) * kHeadDim + 64 * hf);
 #pragma unroll
@@ -192,7 +204,7 @@ __global__ void __launch_bounds__(kFaThreads, 2)
     // K of page i lives in stage i % 2 until S_i is done, V until PV_i is.
     if ((tid & 31) == 0 && np > 0) {
       auto page_row = [&](int i) {
-        return ((p.layer * p.n_pages + p.page_table[t_lo + i]) * p.n_kv + g) * kPage;
+        return ((p.layer * p.n_pages + ptab[t_lo + i]) * p.n_kv + g) * kPage;
       };
       auto issue_k = [&](int i) {
         const int st = i % kFaStages;
@@ -257,7 +269,7 @@ __global__ void __launch_bounds__(kFaThreads, 2)
   } else {
     // ---- softmax warps: thread (r, hf) owns 32 positions of each page of row r
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const int lim = start + (row0 + r < M_rows ? row0 + r : M_rows - 1) / G;
+    const int lim = start + (row0 + r < span_rows ? row0 + r : span_rows - 1) / G;
     float m = -INFINITY, l = 0.f;  // l: this half's share of the row sum
     for (int i = 0; i < np; ++i) {
       const int sb = i & 1;
@@ -328,7 +340,7 @@ __global__ void __launch_bounds__(kFaThreads, 2)
     }
     named_barrier_sync(1, kFaSoftmaxWarps * 32);
     l += xch[0][hf ^ 1][r];
-    const int rr = row0 + r;
+    const int rr = grow0 + row0 + r;  // global query row
     const size_t part_stride = kHeadDim + 2;
     float* prow = nullptr;  // this row's (m, l) slot of the split partials
     if (r < rows_here && nsplit > 1)
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__(kFaThreads, 2)
     named_barrier_sync(1, kFaSoftmaxWarps * 32);
     const int lane = tid & 31;
     for (int row = warp; row < rows_here; row += kFaSoftmaxWarps) {
-      const int rw = row0 + row;
+      const int rw = grow0 + row0 + row;  // global query row
       const float* src = stage + row * kStageLd;
       if (nsplit == 1) {
         const int tok = rw / G, j = rw % G;
@@ -400,7 +412,7 @@ int attn_umma_splits(int n_kv, int q_tiles, int T, int num_sms) {
 int attn_umma_q_tiles(int M_tokens, int G) { return (M_tokens * G + kFaRows - 1) / kFaRows; }
 
 cudaError_t attn_umma_launch(const void* tmK, const void* tmV, const AttnParams& p, int M_tokens,
-                             int nsplit, cudaStream_t stream) {
+                             int nsplit, cudaStream_t stream, int n_items) {
   const int G = p.n_heads / p.n_kv;
   const int M_rows = M_tokens * G;
   static bool attr = false;
@@ -411,7 +423,7 @@ cudaError_t attn_umma_launch(const void* tmK, const void* tmV, const AttnParams&
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_kv, nsplit, (M_rows + kFaRows - 1) / kFaRows);
+  cfg.gridDim = dim3(p.n_kv, nsplit, p.spans ? n_items : (M_rows + kFaRows - 1) / kFaRows);
   cfg.blockDim = dim3(kFaThreads);
   cfg.dynamicSmemBytes = kFaSmem;
   cfg.stream = stream;

@@ -94,6 +94,10 @@ struct AttnParams {
   int sep_merge;             // prefill: leave split partials for attn_merge_launch
   int p_hi_only;             // prefill: P.V with bf16 P only (no hi/lo split)
   DecodeState* st;           // decode: ctx_len / page table from here
+  // multi-sequence prefill (umma kernel): per grid-z item (first token, tokens,
+  // start position, query tile of the span) and that span's page table
+  const int4* spans;
+  const int* const* span_tables;
 };
 
 cudaError_t attn_decode_launch(const AttnParams& p, cudaStream_t stream, bool pdl);
@@ -109,7 +113,7 @@ cudaError_t attn_prefill_launch(const AttnParams& p, int M, cudaStream_t stream)
 // tcgen05 flash attention (attention_umma.cu); tmK / tmV: 128-B swizzled tensor
 // maps over the K / V pools viewed as [rows = L*n_pages*n_kv*64, 128], box 64x64
 cudaError_t attn_umma_launch(const void* tmK, const void* tmV, const AttnParams& p, int M_tokens,
-                             int nsplit, cudaStream_t stream);
+                             int nsplit, cudaStream_t stream, int n_items = 0);
 int attn_umma_splits(int n_kv, int q_tiles, int T, int num_sms);
 int attn_umma_q_tiles(int M_tokens, int G);
 

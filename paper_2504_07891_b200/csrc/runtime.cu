@@ -41,10 +41,11 @@ static int fail(int code, const std::string& msg) {
 
 constexpr int kPrefillSplitsMax = 8;
 constexpr int kAttnPrefillSplit = 16;
+constexpr int kAttnItemsMax = 4096;  // (span, query tile) items of one multi-sequence pass
 
 struct Layout {  // workspace carve-up (byte offsets)
   size_t st, h, x, q, attn, act, part, apart, actr, lm_v1, lm_v2, lm_i1, lm_ctr, logits, ro_cnt,
-      mk_maps, mk_layers, mk_h, mk_part, mk_apart, mk_lm, mk_prof, mk_ctab, tp_delta, tp_small,
+      mk_maps, mk_layers, mk_h, mk_part, mk_apart, mk_lm, mk_prof, mk_ctab, tp_delta, tp_small, attn_items, attn_tabs,
       total;
   int mk_maxj;
   int nsplit_decode;
@@ -104,6 +105,8 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
   L.mk_apart = take((size_t)num_sms * 8 * 130 * 4);
   L.mk_lm = take((size_t)num_sms * 3 * 4);
   L.mk_prof = take((size_t)SR_PROF_EVENTS * 8);
+  L.attn_items = take((size_t)kAttnItemsMax * 16);  // int4 per (span, query tile)
+  L.attn_tabs = take((size_t)kAttnItemsMax * 8);    // page table pointer per item
   L.mk_ctab = take(3 * 256 * 2 + 64 * 4);
   // tensor parallelism: the all-reduced row-parallel output, exchange buffers
   L.tp_delta = take(T * d.d_model * 4);
@@ -451,6 +454,29 @@ struct Model {
   int run_layers(const int* ids, int M, const SeqSpan* spans, int n_spans, const int* tok_meta,
                  cudaStream_t s) {
     SR_CK(embed_norm_launch(ids, M, embed, d.d_model, lw(0, LN1), d.rms_eps, h, x, s));
+    // several spans on the tcgen05 attention: one launch per layer over a
+    // (span, query tile) item table
+    const bool multi = n_spans > 1 && attn_umma && !attn_simt;
+    int n_items = 0, t_max = 0;
+    if (multi) {
+      const int G = d.n_heads / d.n_kv_heads;
+      std::vector<int4> items;
+      std::vector<const int*> tabs;
+      for (int k = 0; k < n_spans; ++k) {
+        const int tiles = attn_umma_q_tiles(spans[k].M, G);
+        for (int t = 0; t < tiles; ++t) {
+          items.push_back(make_int4(spans[k].row0, spans[k].M, spans[k].start, t));
+          tabs.push_back(spans[k].page_table);
+        }
+        t_max = std::max(t_max, spans[k].start + spans[k].M);
+      }
+      n_items = (int)items.size();
+      if (n_items > kAttnItemsMax) return fail(SR_E_CAPACITY, "too many attention items");
+      SR_CK(cudaMemcpyAsync(ws + L.attn_items, items.data(), items.size() * sizeof(int4),
+                            cudaMemcpyHostToDevice, s));
+      SR_CK(cudaMemcpyAsync(ws + L.attn_tabs, tabs.data(), tabs.size() * sizeof(const int*),
+                            cudaMemcpyHostToDevice, s));
+    }
     for (int l = 0; l < d.n_layers; ++l) {
       // qkv
       int rc = gemm(ACT_X, l * 4 + 0, x, lw(l, WQKV), M, qkv_rows, d.d_model, s);
@@ -464,8 +490,28 @@ struct Model {
       ep.layer = l;
       SR_CK(epi_qkv_launch(ep, s));
       watch(s, "qkv gemm+epi", l, M, last_splits);
-      // attention, per sequence
-      for (int k = 0; k < n_spans; ++k) {
+      // attention: all spans in one launch, or per sequence
+      if (multi) {
+        AttnParams a{};
+        a.q = q;
+        a.out = attn;
+        a.k_pool = k_pool;
+        a.v_pool = v_pool;
+        a.page_table = spans[0].page_table;
+        a.part = apart;
+        a.counters = actr;
+        a.layer = l;
+        a.n_pages = d.n_pages;
+        a.n_heads = d.n_heads;
+        a.n_kv = d.n_kv_heads;
+        a.spans = reinterpret_cast<const int4*>(ws + L.attn_items);
+        a.span_tables = reinterpret_cast<const int* const*>(ws + L.attn_tabs);
+        a.nsplit = std::min(kAttnPrefillSplit, attn_umma_splits(d.n_kv_heads, n_items, t_max, num_sms));
+        SR_CK(attn_umma_launch(&kvmaps[0].m, &kvmaps[1].m, a, M, a.nsplit, s, n_items));
+        if (a.nsplit > 1) SR_CK(attn_merge_launch(a, M, a.nsplit, s));
+        watch(s, "attn_prefill_umma (spans)", l, M, a.nsplit);
+      }
+      for (int k = 0; k < (multi ? 0 : n_spans); ++k) {
         const SeqSpan& sp = spans[k];
         AttnParams a{};
         a.q = q + (size_t)sp.row0 * q_dim;
