@@ -182,8 +182,9 @@ def run_ours(args) -> None:
         from paper_2504_07891_b200.backend import TensorParallel
 
         base_tp = TensorParallel.from_dist() if dist is not None else TensorParallel.single()
+    extra = {"n_streams": 2 * args.batch + 2, "max_tokens": 1024} if args.batch > 1 else {}
     small, base = build_pair(args.pair, seed=args.seed, max_ctx=args.budget + 512,
-                             threshold=args.threshold, base_tp=base_tp)
+                             threshold=args.threshold, base_tp=base_tp, **extra)
     base.verify_template = args.verify_template
     if args.spec_gamma > 0:  # SpecReason+Decode: the draft proposes tokens inside base fallback
         base.attach_speculator(small, gamma=args.spec_gamma)
@@ -192,10 +193,31 @@ def run_ours(args) -> None:
                        token_budget=args.budget, max_step_tokens=args.max_step_tokens)
     # DP: independent problems per rank; TP: every rank drives the same one
     problems = [(0 if args.mode == "tp" else rank) * 1000 + i for i in range(64)]
-    src = StepSource(small, base, cfg, problems, vocab)
+    sched = None
+    if args.batch > 1:  # B trajectories, each on its own thread, batched device passes
+        from paper_2504_07891_b200.batching import BatchScheduler
 
-    for _ in range(args.warmup):
-        src.step()
+        sched = BatchScheduler(small, base)
+        srcs = [StepSource(sched.small, sched.base, cfg, problems[k::args.batch], vocab)
+                for k in range(args.batch)]
+        per = -(-args.steps // args.batch)
+
+        def run_steps(n):
+            res = sched.run([lambda s_, b_, src=src: [src.step() for _ in range(n)] for src in srcs])
+            bad = [r for r in res if isinstance(r, BaseException)]
+            if bad:
+                raise bad[0]
+            return [o for r in res for o in r]
+
+        class _Multi:  # StepSource-like view for the shared reporting below
+            trajectories = property(lambda self: sum(x.trajectories for x in srcs))
+
+        src = _Multi()
+        run_steps(max(1, -(-args.warmup // args.batch)))
+    else:
+        src = StepSource(small, base, cfg, problems, vocab)
+        for _ in range(args.warmup):
+            src.step()
 
     stream = torch.cuda.current_stream()
     s0 = (small.engine.stats.snapshot(), base.engine.stats.snapshot())
@@ -206,13 +228,17 @@ def run_ours(args) -> None:
     outcomes = []
     with ClockSampler(local) as clocks:
         e0.record(stream)
-        for _ in range(args.steps):
-            outcomes.append(src.step())
+        if sched is not None:
+            outcomes = run_steps(per)
+        else:
+            for _ in range(args.steps):
+                outcomes.append(src.step())
         e1.record(stream)
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     wall_ms = e0.elapsed_time(e1)
+    n_steps = len(outcomes)  # --batch B runs ceil(steps / B) steps on each trajectory
     ds = small.engine.stats.minus(s0[0])
     db = base.engine.stats.minus(s0[1])
 
@@ -236,30 +262,32 @@ def run_ours(args) -> None:
         "value": round(tot_tokens / (max_dev_ms * 1e-3), 2),
         "unit": UNIT,
         "n_gpus": world,
-        "steps": args.steps,
+        "steps": n_steps,
         "warmup": args.warmup,
-        "ms_per_step": round(max_wall_ms / args.steps, 3),
+        "ms_per_step": round(max_wall_ms / n_steps, 3),
         "higher_is_better": True,
         "scaling": "weak" if args.mode == "dp" else "strong",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights, seeded 64-word problems)",
-        "config": {"workload": WORKLOADS[args.pair], "pair": args.pair, "threshold": args.threshold,
+        "config": {"workload": WORKLOADS[args.pair].replace("batch 1", f"batch {args.batch}"), "pair": args.pair, "threshold": args.threshold,
                    "verify_template": args.verify_template, "spec_gamma": args.spec_gamma,
                    "token_budget": args.budget, "max_step_tokens": args.max_step_tokens,
-                   "batch": 1, "parallelism": (f"dp{world} (independent problems per GPU)"
+                   "batch": args.batch, "parallelism": (f"dp{world} (independent problems per GPU"
+                                               + (f", {args.batch} concurrent trajectories per GPU "
+                                                  "sharing batched device passes)" if args.batch > 1 else ")")
                                                if args.mode == "dp" else
                                                f"tp{world} (base sharded, NCCL all-reduce; draft replicated)"),
                    "l2": "weights (17 GB) exceed L2 (126 MB): no flush needed"},
         "e2e": {"value": round(tot_tokens / (max_wall_ms * 1e-3), 2), "unit": UNIT,
-                "ms_per_step": round(max_wall_ms / args.steps, 3),
-                "h2d_bytes_per_step": round((ds.h2d_bytes + db.h2d_bytes) / args.steps),
-                "d2h_bytes_per_step": round((ds.d2h_bytes + db.d2h_bytes) / args.steps)},
+                "ms_per_step": round(max_wall_ms / n_steps, 3),
+                "h2d_bytes_per_step": round((ds.h2d_bytes + db.h2d_bytes) / n_steps),
+                "d2h_bytes_per_step": round((ds.d2h_bytes + db.d2h_bytes) / n_steps)},
         "breakdown_ms_per_step": {
-            "speculate": round(1e3 * sum(x.speculate_s for x in lat) / args.steps, 3),
-            "verify": round(1e3 * sum(x.verify_s for x in lat) / args.steps, 3),
-            "fallback": round(1e3 * sum(x.fallback_s for x in lat) / args.steps, 3),
-            "device": round(dev_ms / args.steps, 3)},
+            "speculate": round(1e3 * sum(x.speculate_s for x in lat) / n_steps, 3),
+            "verify": round(1e3 * sum(x.verify_s for x in lat) / n_steps, 3),
+            "fallback": round(1e3 * sum(x.fallback_s for x in lat) / n_steps, 3),
+            "device": round(dev_ms / n_steps, 3)},
         "loop": {"tokens": tokens, "accepted_fraction": round(n_spec / len(outcomes), 3),
                  "trajectories": src.trajectories,
                  "draft_decode_ms_per_token": round(ds.decode_ms / max(1, ds.decode_tokens), 4),
@@ -282,7 +310,7 @@ def run_ours(args) -> None:
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(args, outcomes_stats=(ds, db, tokens, args.steps))
+        result["cpu_baseline"] = cpu_baseline(args, outcomes_stats=(ds, db, tokens, n_steps))
     print(json.dumps(result), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -428,7 +456,7 @@ def run_reference(args) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / len(timed), 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": WORKLOADS[args.pair], "pair": args.pair,
+        "data": "synthetic", "config": {"workload": WORKLOADS[args.pair].replace("batch 1", f"batch {args.batch}"), "pair": args.pair,
                                         "threshold": args.threshold, "token_budget": args.budget},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{engine_kind} driving the CPU oracle; per-token CPU costs of "
@@ -463,6 +491,9 @@ def main() -> None:
                     help="v2: prefix-sharing verification prompt (not the reference wording)")
     ap.add_argument("--spec-gamma", type=int, default=0,
                     help="token-level speculation inside base generation (0 = off)")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="trajectories per GPU run concurrently with batched device passes "
+                         "(SURVEY 8f-2; config C5 uses 8); 1 = the C2 batch-1 workload")
     ap.add_argument("--mode", default="dp", choices=["dp", "tp"],
                     help="multi-GPU: dp = independent problems per rank (C5), "
                          "tp = base model tensor-parallel over the ranks (C4)")

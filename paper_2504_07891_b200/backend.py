@@ -364,6 +364,9 @@ class NativeEngine:
         self.stats.calls += 1
         self.stats.prefill_ms += m.timing().prefill_ms
         self.stats.prefill_tokens += rows
+        self.stats.launches += 9 * self.spec.n_layers + 3 + n
+        self.stats.h2d_bytes += 12 * rows
+        self.stats.d2h_bytes += 16 * n
         res = []
         for i, (st, suf) in enumerate(zip(streams, suffixes)):
             st.ids.extend(suf)
@@ -404,6 +407,9 @@ class NativeEngine:
                 self.stats.calls += 1
                 self.stats.prefill_ms += m.timing().prefill_ms
                 self.stats.prefill_tokens += rows
+                self.stats.launches += 9 * self.spec.n_layers + 3
+                self.stats.h2d_bytes += 12 * rows
+                self.stats.d2h_bytes += 4 * n
             nxt = []
             for k, i in enumerate(live):
                 streams[i].ids.extend(feed[i])
