@@ -97,6 +97,16 @@ class RefEngine:
     def score_batch(self, streams, suffixes, threshold: int) -> list[Readout]:
         return [self.score(s, suf, threshold) for s, suf in zip(streams, suffixes)]
 
+    def step_batch(self, streams, feeds, room: int = 0) -> list[int]:
+        out = []
+        for st, f in zip(streams, feeds):
+            logits = self.model.forward(st.handle, list(f))
+            st.ids.extend(f)
+            t, m = argmax_margin(masked(logits, self.vocab.n_text))
+            self.margins.append(m)
+            out.append(t)
+        return out
+
     def generate_batch(self, streams, suffixes, max_new: int, stop: tuple[str, ...]):
         return [self.generate(s, suf, max_new, stop) for s, suf in zip(streams, suffixes)]
 

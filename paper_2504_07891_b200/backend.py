@@ -100,6 +100,11 @@ class DeviceModel:
         self.margin_dev = torch.zeros(max_new, dtype=torch.float32, device=self.device)
         self.out_host = torch.empty(2 + max_new, dtype=torch.int32, pin_memory=True)
         self.margin_host = torch.empty(max_new, dtype=torch.float32, pin_memory=True)
+        # multi-sequence passes: (position, page) per row, outputs per sequence
+        self.meta_host = torch.empty(2 * max_tokens, dtype=torch.int32, pin_memory=True)
+        self.meta_dev = torch.empty(2 * max_tokens, dtype=torch.int32, device=self.device)
+        self.batch_out = torch.zeros(4 * 64, dtype=torch.int32, device=self.device)
+        self.batch_margins = torch.zeros(64, dtype=torch.float32, device=self.device)
         self.readout_dev = torch.zeros(4, dtype=torch.int32, device=self.device)
         self.readout_host = torch.empty(4, dtype=torch.int32, pin_memory=True)
 
@@ -315,8 +320,10 @@ class NativeEngine:
             flat.extend(suf)
         n = len(streams)
         ids_ptr = m.upload_ids(flat)
-        meta_t = torch.as_tensor(meta, dtype=torch.int32).pin_memory()
-        meta_dev = meta_t.to(m.device, non_blocking=True)
+        k = len(meta)
+        m.meta_host[:k] = torch.as_tensor(meta, dtype=torch.int32)
+        m.meta_dev[:k].copy_(m.meta_host[:k], non_blocking=True)
+        meta_dev = m.meta_dev
         tables = (C.c_void_p * n)(*[st.handle.table_dev.data_ptr() for st in streams])
         return (n, tables, (C.c_int32 * n)(*starts), (C.c_int32 * n)(*counts),
                 C.c_void_p(ids_ptr), meta_dev, len(flat))
@@ -355,12 +362,12 @@ class NativeEngine:
     def _score_pass(self, streams, suffixes, threshold: int) -> list[Readout]:
         m = self.model
         n, tables, starts, counts, ids, meta_dev, rows = self._batch(streams, suffixes)
-        out = torch.zeros(4 * n, dtype=torch.int32, device=m.device)
+        out = m.batch_out
         native.check("sr_score_batch", m.lib.sr_score_batch(
             m.handle, n, tables, starts, counts, ids, C.c_void_p(meta_dev.data_ptr()),
             C.c_void_p(self.first_digit.data_ptr()), int(threshold), C.c_void_p(out.data_ptr()),
             m.stream_ptr))
-        host = out.cpu()
+        host = out[:4 * n].cpu()
         self.stats.calls += 1
         self.stats.prefill_ms += m.timing().prefill_ms
         self.stats.prefill_tokens += rows
@@ -375,44 +382,54 @@ class NativeEngine:
                                margin=r[2:3].view(torch.float32).item(), argmax=int(r[3])))
         return res
 
+    def step_batch(self, streams: Sequence[Stream], feeds: Sequence[Sequence[int]],
+                   room: int = 0) -> list[int]:
+        """One greedy token for each stream after feeding ``feeds[i]`` (prompt
+        rows or the previous token), in as few ``sr_step_batch`` passes as
+        max_tokens allows; the fed tokens are committed to the streams.
+        ``room`` positions are reserved past the feed for later tokens."""
+        m = self.model
+        feeds = [list(f) for f in feeds]
+        for i, f in enumerate(feeds):  # beyond one pass: all but the last token on the chunked path
+            if len(f) > m.max_tokens:
+                self.prefill(streams[i], f[:-1])
+                feeds[i] = f[-1:]
+        out, margins = m.batch_out, m.batch_margins
+        toks: list[int] = [0] * len(streams)
+        for group in self._passes([len(f) for f in feeds]):
+            n, tables, starts, counts, ids, meta_dev, rows = self._batch(
+                [streams[i] for i in group], [feeds[i] for i in group], room=room)
+            native.check("sr_step_batch", m.lib.sr_step_batch(
+                m.handle, n, tables, starts, counts, ids, C.c_void_p(meta_dev.data_ptr()),
+                C.c_void_p(out.data_ptr()), C.c_void_p(margins.data_ptr()), m.stream_ptr))
+            for i, t in zip(group, out[:n].tolist()):
+                toks[i] = t
+            self.stats.calls += 1
+            self.stats.prefill_ms += m.timing().prefill_ms
+            self.stats.prefill_tokens += rows
+            self.stats.launches += 9 * self.spec.n_layers + 3
+            self.stats.h2d_bytes += 12 * rows
+            self.stats.d2h_bytes += 4 * n
+        for st, f in zip(streams, feeds):
+            st.ids.extend(f)
+        return toks
+
     def generate_batch(self, streams: Sequence[Stream], suffixes: Sequence[Sequence[int]],
                        max_new: int, stop: tuple[str, ...]) -> list[tuple[list[int], int]]:
         """Greedy ``generate`` for several streams, one batched step per token
-        (``sr_step_batch``): each step streams the weights once for every live
+        (``step_batch``): each step streams the weights once for every live
         sequence.  Finished sequences leave the batch."""
         from .host import finish_of
 
-        m = self.model
         classes = self.vocab.token_classes(stop, self.n_ids)
         live = list(range(len(streams)))
         gens: list[list[int]] = [[] for _ in streams]
         feed = [list(s) for s in suffixes]
-        out = torch.zeros(len(streams), dtype=torch.int32, device=m.device)
-        margins = torch.zeros(len(streams), dtype=torch.float32, device=m.device)
         self.last_margins = []
-        for i in live:  # prompts beyond one pass: all but the last token on the chunked path
-            if len(feed[i]) > m.max_tokens:
-                self.prefill(streams[i], feed[i][:-1])
-                feed[i] = feed[i][-1:]
         while live:
-            toks = []
-            for group in self._passes([len(feed[i]) for i in live]):
-                idx = [live[g] for g in group]
-                n, tables, starts, counts, ids, meta_dev, rows = self._batch(
-                    [streams[i] for i in idx], [feed[i] for i in idx], room=max_new)
-                native.check("sr_step_batch", m.lib.sr_step_batch(
-                    m.handle, n, tables, starts, counts, ids, C.c_void_p(meta_dev.data_ptr()),
-                    C.c_void_p(out.data_ptr()), C.c_void_p(margins.data_ptr()), m.stream_ptr))
-                toks += out[:n].tolist()
-                self.stats.calls += 1
-                self.stats.prefill_ms += m.timing().prefill_ms
-                self.stats.prefill_tokens += rows
-                self.stats.launches += 9 * self.spec.n_layers + 3
-                self.stats.h2d_bytes += 12 * rows
-                self.stats.d2h_bytes += 4 * n
+            toks = self.step_batch([streams[i] for i in live], [feed[i] for i in live], room=max_new)
             nxt = []
             for k, i in enumerate(live):
-                streams[i].ids.extend(feed[i])
                 gens[i].append(toks[k])
                 if classes[toks[k]] in (CLASS_STOP, CLASS_END_THINK) or len(gens[i]) >= max_new:
                     continue

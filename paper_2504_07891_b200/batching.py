@@ -7,9 +7,9 @@ thread-safe (``base.py:80-81``).  ``BatchScheduler`` keeps that contract and
 adds what a GPU needs to profit from it: each trajectory thread calls a proxy
 backend, the proxy parks the request, and a dispatcher thread releases the
 parked requests as batched device passes -- ``generate_steps`` (one weight
-stream per token for every live sequence) and ``score_steps`` (one prefill
-pass over every candidate step).  Requests are grouped by (backend, kind,
-stop list, max_tokens); a group larger than the backend's KV streams is split.
+stream per token for every live sequence, continuously batched: a new
+generation joins the running ones at the next token) and ``score_steps`` (one
+prefill pass over every candidate step that is waiting).
 
 Trajectory semantics do not change: each request still gets exactly the
 result its backend's single-request call returns (up to flagged near-ties,
@@ -103,43 +103,130 @@ class BatchScheduler:
         self._thread.join()
 
     # -- dispatcher ------------------------------------------------------------
+    # Continuous batching: generations are opened as their requests arrive and
+    # every live generation of a backend advances one token per device pass
+    # (``engine.step_batch``: new prompts and single-token feeds share the
+    # pass); scoring requests that arrive meanwhile run between two steps as
+    # one ``score_steps`` pass.
     def _loop(self) -> None:
+        live: dict[int, tuple[Any, list]] = {}  # id(backend) -> (backend, open generations)
         while True:
             with self._cv:
-                while not self._pending and not self._stop:
-                    self._cv.wait()
-                if self._stop and not self._pending:
-                    return
-                deadline = time.monotonic() + self.linger_s
-                while len(self._pending) < self._active and not self._stop:
-                    left = deadline - time.monotonic()
-                    if left <= 0:
-                        break
-                    self._cv.wait(left)
+                busy = any(gs for _, gs in live.values())
+                if not busy:
+                    while not self._pending and not self._stop:
+                        self._cv.wait()
+                    if self._stop and not self._pending:
+                        return
+                    deadline = time.monotonic() + self.linger_s
+                    while len(self._pending) < self._active and not self._stop:
+                        left = deadline - time.monotonic()
+                        if left <= 0:
+                            break
+                        self._cv.wait(left)
                 batch, self._pending = self._pending, []
-            self._dispatch(batch)
+            self._scores([it for it in batch if it[1] == "score"])
+            deferred = self._admit([it for it in batch if it[1] == "gen"], live)
+            if deferred:
+                with self._cv:
+                    self._pending = deferred + self._pending
+            for backend, gens in live.values():
+                if gens:
+                    self._step(backend, gens)
 
-    def _dispatch(self, batch) -> None:
-        groups: dict[tuple, list] = {}
-        for backend, kind, req, fut in batch:
-            key = (id(backend), kind) + ((tuple(req.stop), req.max_tokens) if kind == "gen" else ())
-            groups.setdefault(key, []).append((backend, kind, req, fut))
-        for items in groups.values():
-            backend, kind = items[0][0], items[0][1]
-            cap = len(backend.pool.streams)  # one KV stream per request of a pass
-            for i in range(0, len(items), cap):
-                chunk = items[i:i + cap]
+    def _scores(self, items) -> None:
+        groups: dict[int, list] = {}
+        for it in items:
+            groups.setdefault(id(it[0]), []).append(it)
+        for chunk_all in groups.values():
+            backend = chunk_all[0][0]
+            cap = len(backend.pool.streams)
+            for i in range(0, len(chunk_all), cap):
+                chunk = chunk_all[i:i + cap]
                 reqs = [it[2] for it in chunk]
                 try:
-                    if len(reqs) == 1:
-                        one = (backend.generate_step if kind == "gen" else backend.score_step)(reqs[0])
-                        res: list = [one]
-                    elif kind == "gen":
-                        res = backend.generate_steps(reqs)
-                    else:
-                        res = backend.score_steps(reqs)
+                    res = ([backend.score_step(reqs[0])] if len(reqs) == 1
+                           else backend.score_steps(reqs))
                 except BaseException as exc:
                     res = [exc] * len(chunk)
                 self.batches.append(len(chunk))
-                for (_, _, _, fut), r in zip(chunk, res):
-                    fut.set_result(r)
+                for it, r in zip(chunk, res):
+                    it[3].set_result(r)
+
+    def _admit(self, items, live) -> list:
+        """Open generations for new requests; those that find no free KV
+        stream wait for the next round."""
+        deferred = []
+        for backend, kind, req, fut in items:
+            _, gens = live.setdefault(id(backend), (backend, []))
+            if len(gens) >= len(backend.pool.streams):
+                deferred.append((backend, kind, req, fut))
+                continue
+            try:
+                with backend._lock:
+                    g = backend.gen_open(req, exclude=[x["stream"] for x in gens])
+            except BaseException as exc:
+                fut.set_result(exc)
+                continue
+            g["fut"] = fut
+            gens.append(g)
+        return deferred
+
+    # a lone generation runs `solo_tokens` at a time on the single-stream
+    # decode path (the persistent kernel) instead of one-token batched passes
+    solo_tokens = 16
+
+    def _step(self, backend, gens: list) -> None:
+        if len(gens) == 1 and hasattr(backend.engine, "generate"):
+            return self._solo(backend, gens)
+        try:
+            with backend._lock:
+                toks = backend.engine.step_batch([g["stream"] for g in gens],
+                                                 [g["feed"] for g in gens],
+                                                 room=max(g["max"] - len(g["gen"]) for g in gens))
+        except BaseException as exc:
+            err = exc
+            if isinstance(exc, RuntimeError) and type(exc).__name__ == "NativeError":
+                err = backend._device_error(exc)
+            for g in gens:
+                g["fut"].set_result(err)
+            gens.clear()
+            return
+        self.batches.append(len(gens))
+        keep = []
+        for g, t in zip(gens, toks):
+            g["gen"].append(t)
+            if backend.gen_done(g):
+                try:
+                    g["fut"].set_result(backend.gen_close(g))
+                except BaseException as exc:
+                    g["fut"].set_result(exc)
+            else:
+                g["feed"] = [t]
+                keep.append(g)
+        gens[:] = keep
+
+    def _solo(self, backend, gens: list) -> None:
+        g = gens[0]
+        n = min(self.solo_tokens, g["max"] - len(g["gen"]))
+        try:
+            with backend._lock:
+                # stop ids end the chunk exactly as they end a generation
+                toks, _ = backend.engine.generate(g["stream"], g["feed"], n, g["stop"])
+        except BaseException as exc:
+            err = exc
+            if isinstance(exc, RuntimeError) and type(exc).__name__ == "NativeError":
+                err = backend._device_error(exc)
+            g["fut"].set_result(err)
+            gens.clear()
+            return
+        self.batches.append(1)
+        g["gen"].extend(toks)
+        if backend.gen_done(g):
+            try:
+                g["fut"].set_result(backend.gen_close(g))
+            except BaseException as exc:
+                g["fut"].set_result(exc)
+            gens.clear()
+        else:
+            g["feed"] = [toks[-1]]

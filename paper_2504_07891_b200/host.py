@@ -325,6 +325,38 @@ class ModelBackend(Backend):
         return [T.UtilityScore(r.score) if r.score >= 0 else
                 T.ScoreParseFailure("no digit in the top-10 or the sampled token") for r in rs]
 
+    # continuous batching (batching.BatchScheduler): a generation is opened,
+    # stepped together with other streams' generations, and closed
+    def gen_open(self, request: GenerationRequest, exclude=()) -> dict:
+        ids = self._prompts.encode(request.prompt)
+        stream, keep = self.pool.acquire(ids, exclude=exclude)
+        self.engine.truncate(stream, keep)
+        n_rows = getattr(self.engine, "n_ids", None) or self.engine.spec.vocab_rows
+        return {"stream": stream, "feed": ids[keep:], "gen": [], "max": request.max_tokens,
+                "stop": tuple(request.stop),
+                "classes": self.vocab.token_classes(tuple(request.stop), n_rows),
+                "t0": time.monotonic()}
+
+    def gen_done(self, g: dict) -> bool:
+        return (g["gen"] and g["classes"][g["gen"][-1]] in (CLASS_STOP, CLASS_END_THINK)) \
+            or len(g["gen"]) >= g["max"]
+
+    def gen_close(self, g: dict):
+        T = self.types
+        gen = g["gen"]
+        finish = finish_of(gen, g["classes"])
+        if finish == FINISH_END_THINK:
+            text_ids, reason = gen[:-1], T.FinishReason.END_THINK
+        elif finish == FINISH_STOP:
+            text_ids, reason = gen, T.FinishReason.STOP
+        else:
+            text_ids, reason = gen, T.FinishReason.LENGTH
+        text = self.vocab.render(text_ids)
+        if not text and reason == T.FinishReason.STOP:
+            raise T.BackendMisbehavior("empty text with finish_reason stop")
+        return T.GenerationResult(text=text, token_count=len(text_ids), finish_reason=reason,
+                                  measured_latency_s=time.monotonic() - g["t0"])
+
     def generate_steps(self, requests: Sequence[GenerationRequest]) -> list:
         """``generate_step`` for several independent requests, decoded together
         (the engine's ``generate_batch``: one weight stream per token for all
