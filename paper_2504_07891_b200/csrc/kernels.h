@@ -177,9 +177,12 @@ cudaError_t epi_resid_norm_launch(const EpiParams& p, cudaStream_t stream);
 cudaError_t epi_glu_launch(const EpiParams& p, cudaStream_t stream);
 
 // per-row greedy choice over split LM-head partials (token-level speculation)
+// (rows <= 16 with scratch: each row split over 16 CTAs; cv1/cv2/ci1 hold
+// rows*16 chunk results, ctr one zeroed counter per row)
 cudaError_t rows_argmax_launch(const float* part, int splits, size_t stride, int rows, int N,
                                int n_valid, int base, int32_t* out_ids, float* margins,
-                               cudaStream_t stream);
+                               cudaStream_t stream, float* cv1 = nullptr, float* cv2 = nullptr,
+                               int* ci1 = nullptr, unsigned* ctr = nullptr, int scratch = 0);
 
 // verify readout over fp32 logits [V]
 struct ReadoutParams {

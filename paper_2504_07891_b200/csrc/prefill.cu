@@ -390,9 +390,60 @@ __global__ void __launch_bounds__(1024) rows_argmax_kernel(const float* part, in
   }
 }
 
+// Few rows (batched decode steps): each row's vocabulary is split over
+// kArgmaxChunks CTAs; the last CTA of a row merges the chunk top-2s in chunk
+// order (deterministic, ties: lower id) and resets the row's counter.
+constexpr int kArgmaxChunks = 16;
+__global__ void __launch_bounds__(512) rows_argmax_chunk_kernel(
+    const float* part, int splits, size_t stride, int N, int n_valid, int base, int32_t* out_ids,
+    float* margins, float* cv1, float* cv2, int* ci1, unsigned* ctr) {
+  grid_wait();
+  __shared__ float s1[16], s2[16];
+  __shared__ int si[16];
+  __shared__ bool last;
+  const int r = blockIdx.x, c = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n_valid + kArgmaxChunks - 1) / kArgmaxChunks;
+  const int v0 = c * per, v1 = min(n_valid, v0 + per);
+  Top2 b;
+  b.init();
+  for (int v = v0 + tid; v < v1; v += blockDim.x) {
+    float x = 0.f;
+    for (int sp = 0; sp < splits; ++sp) x += __ldcg(part + sp * stride + (size_t)r * N + v);
+    b.push(x, base + v);
+  }
+  warp_top2(b);
+  if (lane == 0) { s1[warp] = b.v1; s2[warp] = b.v2; si[warp] = b.i1; }
+  __syncthreads();
+  if (tid == 0) {
+    Top2 f;
+    f.init();
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) f.merge(s1[w], si[w], s2[w]);
+    const int k = r * kArgmaxChunks + c;
+    cv1[k] = f.v1;
+    cv2[k] = f.v2;
+    ci1[k] = f.i1;
+    __threadfence();
+    last = atomicAdd(ctr + r, 1u) == kArgmaxChunks - 1;
+  }
+  __syncthreads();
+  if (!last || tid != 0) return;
+  __threadfence();
+  Top2 f;
+  f.init();
+  for (int k = r * kArgmaxChunks; k < (r + 1) * kArgmaxChunks; ++k)
+    f.merge(__ldcg(cv1 + k), __ldcg(ci1 + k), __ldcg(cv2 + k));
+  out_ids[r] = f.i1;
+  if (margins) margins[r] = f.v1 - f.v2;
+  ctr[r] = 0u;
+}
+
 cudaError_t rows_argmax_launch(const float* part, int splits, size_t stride, int rows, int N,
                                int n_valid, int base, int32_t* out_ids, float* margins,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, float* cv1, float* cv2, int* ci1,
+                               unsigned* ctr, int scratch) {
+  if (cv1 && rows * kArgmaxChunks <= scratch && rows <= 16)
+    return launch_pdl(rows_argmax_chunk_kernel, dim3(rows, kArgmaxChunks), 512, 0, stream, part,
+                      splits, stride, N, n_valid, base, out_ids, margins, cv1, cv2, ci1, ctr);
   return launch_pdl(rows_argmax_kernel, dim3(rows), 1024, 0, stream, part, splits, stride, N,
                     n_valid, base, out_ids, margins);
 }

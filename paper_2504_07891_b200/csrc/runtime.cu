@@ -1089,7 +1089,8 @@ int sr_verify_tokens(void* model, const int32_t* page_table, int32_t start_pos,
                m->d.d_model, s);
   if (rc) return -rc;
   SR_CK(rows_argmax_launch(m->part, m->last_splits, need, rows, m->d.vocab_rows, m->d.vocab_text,
-                           m->d.vocab_base, out_ids, margins, s));
+                           m->d.vocab_base, out_ids, margins, s, m->lm_v1, m->lm_v2, m->lm_i1,
+                           m->lm_ctr, gemv_max_grid(m->num_sms) + 64));
   SR_CK(cudaEventRecord(m->ev[1], s));
   SR_CK(cudaEventRecord(m->ev[2], s));
   m->timing.prefill_tokens = n_ids;
@@ -1196,7 +1197,8 @@ int sr_step_batch(void* model, int32_t n_seq, const int32_t* const* page_tables,
   if (int rc = batch_forward_last(m, spans, M, ids, tok_meta, s)) return rc;
   const size_t V = m->d.vocab_rows;
   SR_CK(rows_argmax_launch(m->part, m->last_splits, (size_t)n_seq * V, n_seq, (int)V,
-                           m->d.vocab_text, m->d.vocab_base, out_ids, margins, s));
+                           m->d.vocab_text, m->d.vocab_base, out_ids, margins, s, m->lm_v1,
+                           m->lm_v2, m->lm_i1, m->lm_ctr, gemv_max_grid(m->num_sms) + 64));
   SR_CK(cudaEventRecord(m->ev[1], s));
   SR_CK(cudaEventRecord(m->ev[2], s));
   m->timing.prefill_tokens = M;
