@@ -68,6 +68,9 @@ constexpr int kMkThreads = kMkConsumers + 32;
 constexpr int kTR = 32;                    // tile rows
 constexpr int kTC = 256;                   // tile columns (bf16)
 constexpr int kTileBytes = kTR * kTC * 2;  // 16 KB
+#ifndef SR_MK_NB
+#define SR_MK_NB 4
+#endif
 #ifndef SR_MK_UPS
 #define SR_MK_UPS 2
 #endif
@@ -217,7 +220,7 @@ SR_DEV void mk_norm_prologue(const MkParams& p, int mode, int tok, const float* 
   float* hs = tmp;                                            // [d] fp32
   __nv_bfloat16* wsm = reinterpret_cast<__nv_bfloat16*>(tmp + d);  // [d] bf16
   float ss = 0.f;
-  constexpr int kNB = 4;
+  constexpr int kNB = SR_MK_NB;  // rows per thread per load batch
   const size_t cs = (size_t)p.maxj * kTR;
 #pragma unroll 1
   for (int i0 = tid; i0 < d; i0 += kNB * kMkConsumers) {
