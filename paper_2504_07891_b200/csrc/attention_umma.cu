@@ -35,6 +35,7 @@ constexpr int kStageLd = 132;  // fp32 row pitch of the epilogue staging (bank s
 constexpr int kFaSmem = kFaQBytes + kFaStages * kFaStage + 1024;
 static_assert(kFaRows * kStageLd * 4 <= kFaQBytes + kFaStages * kFaStage, "epilogue staging fits");  // 97 KB: 2 CTAs / SM
 constexpr float kFaScaleLog2 = 1.4426950408889634f * 0.08838834764831845f;
+constexpr float kFaLazy = 8.f;  // log2 headroom of the lazy softmax rescale
 
 // byte offset of (row, 16-B chunk) in a 128-B-swizzled K-major [rows x 64] tile
 SR_DEV uint32_t sw128(int row, int chunk) {
@@ -299,9 +300,18 @@ __global__ void __launch_bounds__(kFaThreads, 2)
       xch[sb][hf][r] = mx;
       named_barrier_sync(1, kFaSoftmaxWarps * 32);
       mx = fmaxf(mx, xch[sb][hf ^ 1][r]);
-      const float m_new = fmaxf(m, mx * kFaScaleLog2);
-      const float bse = m_new == -INFINITY ? 0.f : m_new;
-      const float alpha = exp2_ftz(m - bse);  // 0 while nothing was seen
+      // Lazy rescaling: the exponent base m moves only when the row max
+      // exceeds it by more than kFaLazy (P stays <= 2^kFaLazy, harmless in
+      // fp32 and in the bf16 hi/lo pair), so O in TMEM is rarely rescaled --
+      // a rescale reads and writes 64 KB of TMEM per page.  l, O and the split
+      // partial's m all use the same base, so the result is unchanged.
+      const float mxs = mx * kFaScaleLog2;
+      float alpha = 1.f;
+      if (mxs > m + kFaLazy) {  // also the first finite max (m = -inf)
+        alpha = exp2_ftz(m - mxs);  // 0 while nothing was seen
+        m = mxs;
+      }
+      const float bse = m == -INFINITY ? 0.f : m;
       float rs = 0.f;
       float hi[16], lo[16];  // bf16x2 bit patterns
 #pragma unroll
@@ -315,7 +325,6 @@ __global__ void __launch_bounds__(kFaThreads, 2)
         lo[e >> 1] = __uint_as_float(f2_to_bf2(e0 - hv.x, e1 - hv.y));
       }
       l = l * alpha + rs;
-      m = m_new;
       if (i > 0) {  // PV_{i-1} done before O is rescaled
         mbar_wait(&o_done, (uint32_t)((i - 1) & 1));
         __syncwarp();
