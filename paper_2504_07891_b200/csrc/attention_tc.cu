@@ -178,7 +178,6 @@ SR_DEV const __nv_bfloat16* q_row_ptr(const AttnParams& p, int G, int g, int r) 
 __global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams p, int M_rows, int G) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TcaSmem& sm = *reinterpret_cast<TcaSmem*>(smem_raw);
-  __shared__ bool s_last;
 
   grid_launch_dependents();
   grid_wait();
@@ -313,56 +312,7 @@ __global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams
       }
     }
   }
-  if (nsplit == 1 || p.sep_merge) return;  // sep_merge: attn_merge_kernel merges
-
-  // ---- split merge: last CTA of (kv head, query tile) ----
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    unsigned int* ctr = p.counters + (size_t)qt * p.n_kv + g;
-    const unsigned prev = atomicAdd(ctr, 1u);
-    s_last = (prev == (unsigned)nsplit - 1);
-    if (s_last) *ctr = 0u;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  float* wsm = reinterpret_cast<float*>(sm.v[0]);  // [64 rows][kAttnMaxSplit] weights
-  for (int idx = tid; idx < rows_here * nsplit; idx += kTcaThreads) {
-    const int rr = idx / nsplit, sp = idx % nsplit;
-    const float* ps = p.part + ((size_t)(row0 + rr) * nsplit + sp) * part_stride +
-                      (size_t)g * M_rows * nsplit * part_stride;
-    wsm[rr * kAttnMaxSplit + sp] = __ldcg(ps + kHeadDim);
-    wsm[(kRowsPerCta + rr) * kAttnMaxSplit + sp] = __ldcg(ps + kHeadDim + 1);
-  }
-  __syncthreads();
-  for (int rr = tid; rr < rows_here; rr += kTcaThreads) {
-    float M = -INFINITY;
-    for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, wsm[rr * kAttnMaxSplit + sp]);
-    float L = 0.f;
-    for (int sp = 0; sp < nsplit; ++sp) {
-      const float ms = wsm[rr * kAttnMaxSplit + sp];
-      const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
-      L += w * wsm[(kRowsPerCta + rr) * kAttnMaxSplit + sp];
-      wsm[rr * kAttnMaxSplit + sp] = w;
-    }
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    for (int sp = 0; sp < nsplit; ++sp) wsm[rr * kAttnMaxSplit + sp] *= inv;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < rows_here * kHeadDim; idx += kTcaThreads) {
-    const int rr = idx / kHeadDim, d = idx % kHeadDim;
-    const float* base = p.part + ((size_t)(row0 + rr) * nsplit) * part_stride +
-                        (size_t)g * M_rows * nsplit * part_stride + d;
-    float A = 0.f;
-#pragma unroll 8
-    for (int sp = 0; sp < nsplit; ++sp) {
-      const float w = wsm[rr * kAttnMaxSplit + sp];
-      if (w != 0.f) A = fmaf(w, __ldcg(base + (size_t)sp * part_stride), A);
-    }
-    __nv_bfloat16* o = const_cast<__nv_bfloat16*>(q_row_ptr(p, G, g, row0 + rr)) - p.q + p.out;
-    o[d] = __float2bfloat16_rn(A);
-  }
+  // split partials are merged by attn_merge_kernel (grid-wide, fixed split order)
 }
 
 // Split merge for prefill as its own grid-wide kernel: thread = (query row,

@@ -79,7 +79,6 @@ constexpr int kStageBytes = kUPS * kTileBytes;
 constexpr int kMkMaxStages = 13;
 constexpr int kMkMaxGq = 8;
 constexpr int kMkProfEvents = SR_PROF_EVENTS;
-constexpr int kMkNorm = 5120 / kMkConsumers;
 constexpr int kMkAttnScratchFloats =
     kMkMaxGq * 128 + kMkMaxGq * 64 + 3 * kMkMaxGq + kGroups * kMkMaxGq * 128 + 2 * 128;
 constexpr int kMkTab = 256;
@@ -726,7 +725,6 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   __shared__ float s_v1[kMkWarps], s_v2[kMkWarps];
   __shared__ int s_i1[kMkWarps];
   __shared__ int s_tok;
-  __shared__ int s_flag;
   __shared__ uint16_t s_tab[3][kMkTab];  // contributor tables: qkv, o, down
   __shared__ PhaseInfo s_ph[5];
   __shared__ __align__(8) uint64_t kvbar;

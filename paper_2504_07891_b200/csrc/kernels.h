@@ -91,7 +91,6 @@ struct AttnParams {
   unsigned int* counters;    // [M, KV]
   int layer, n_pages, n_heads, n_kv, nsplit;
   int start_pos;             // prefill: position of row 0
-  int sep_merge;             // prefill: leave split partials for attn_merge_launch
   int p_hi_only;             // prefill: P.V with bf16 P only (no hi/lo split)
   DecodeState* st;           // decode: ctx_len / page table from here
   // multi-sequence prefill (umma kernel): per grid-z item (first token, tokens,

@@ -543,7 +543,6 @@ struct Model {
           const int G = d.n_heads / d.n_kv_heads;
           const int q_tiles = (sp.M * G + 63) / 64;
           a.nsplit = std::min(kAttnPrefillSplit, attn_tc_splits(d.n_kv_heads, q_tiles, Tlast, num_sms));
-          a.sep_merge = 1;
           a.p_hi_only = p_hi_only ? 1 : 0;
           SR_CK(attn_tc_launch(a, sp.M, a.nsplit, s, true));
           if (a.nsplit > 1) SR_CK(attn_merge_launch(a, sp.M, a.nsplit, s));
