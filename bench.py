@@ -476,8 +476,9 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     # the loop's step mix (draft steps accepted or regenerated) varies a lot
-    # between random-init trajectories: 120 steps span several of them
-    ap.add_argument("--steps", type=int, default=120)
+    # between random-init trajectories (one C2 trajectory is ~130 steps): 480
+    # steps average over several of them and still run in about a minute
+    ap.add_argument("--steps", type=int, default=480)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pair", default="1.5b+7b")
