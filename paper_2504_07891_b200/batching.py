@@ -96,6 +96,16 @@ class BatchScheduler:
             t.join()
         return out
 
+    def clients(self, n: int) -> "BatchScheduler":
+        """Declare ``n`` client threads that the caller runs itself (e.g. the
+        reference's ``run_sweep(..., parallelism=n)`` thread pool handed
+        ``self.small`` / ``self.base``): a batch is then released once all
+        ``n`` wait.  Undeclare with ``clients(-n)``."""
+        with self._cv:
+            self._active += n
+            self._cv.notify_all()
+        return self
+
     def close(self) -> None:
         with self._cv:
             self._stop = True

@@ -35,3 +35,30 @@ def test_concurrent_trajectories_equal_serial():
         assert key(g) == key(want)
         assert g.metrics.thinking_tokens == want.metrics.thinking_tokens
     assert max(sched.batches) > 1  # requests of different trajectories shared passes
+
+
+def test_reference_run_sweep_through_scheduler(stepspec, tmp_path):
+    """The reference's own thread-pooled sweep driving the proxies."""
+    from stepspec.bench import Knob, SweepSpec, run_sweep
+    from stepspec.core import AcceptanceThreshold as RefThreshold
+    from stepspec.core import EngineConfig as RefConfig
+    from stepspec.core import Scheme
+    from stepspec.simlab import make_tasks
+
+    from paper_2504_07891_b200.host import reference_types
+
+    T = reference_types(stepspec)
+    small = oracle_backend("tiny-draft", BackendRole.SMALL, n_streams=8, types=T)
+    base = oracle_backend("tiny-base", BackendRole.BASE, n_streams=8, types=T)
+    sched = BatchScheduler(small, base).clients(3)
+    try:
+        cfg = RefConfig(threshold=RefThreshold(5), temperature=0.0, token_budget=48,
+                        max_step_tokens=12)
+        res = run_sweep(SweepSpec(knob=Knob.THRESHOLD, values=(5,), base_config=cfg, repeats=1),
+                        make_tasks(3, 2, seed=0), sched.small, sched.base,
+                        schemes=(Scheme.SPEC_REASON,), parallelism=3, output_dir=tmp_path)
+    finally:
+        sched.clients(-3)
+        sched.close()
+    assert len(res.records) == 3
+    assert max(sched.batches) > 1
