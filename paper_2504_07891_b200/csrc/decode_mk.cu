@@ -398,12 +398,15 @@ SR_DEV void mk_fetch_page(const MkParams& p, int layer, int g, int page, uint8_t
 // ticket) merges all splits of g into the bf16 attention output.
 SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_table,
                          const __nv_bfloat16* bias, const uint16_t* tab, int c, int S_a,
-                         int npages, float* sm, uint8_t* kvbuf, uint64_t* kvbar, uint32_t& kvpar) {
+                         int hs, int npages, float* sm, uint8_t* kvbuf, uint64_t* kvbar, uint32_t& kvpar) {
   const int Gq = p.H / p.KV;
-  const int g = c / S_a, s = c % S_a;
+  const int g = c / S_a, s = (c % S_a) / hs, hp = (c % S_a) % hs, PS = S_a / hs;
   if (g >= p.KV) return;  // uniform per CTA
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int p0 = (int)((long long)npages * s / S_a), p1 = (int)((long long)npages * (s + 1) / S_a);
+  const int p0 = (int)((long long)npages * s / PS), p1 = (int)((long long)npages * (s + 1) / PS);
+  // query heads [jl, jh) of the group are this CTA's; the other heads' partial
+  // slots stay (m, l, O) = (-inf, 0, 0), which the combine skips
+  const int jl = Gq * hp / hs, jh = Gq * (hp + 1) / hs;
   float* qs = sm;                              // [8][128]
   float* ps = qs + kMkMaxGq * 128;             // [8][64]
   float* alph = ps + kMkMaxGq * 64;            // [8]
@@ -425,8 +428,8 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
   if (tid == 0) mk_fetch_page(p, layer, g, page_table[p0], kvbuf, kvbar);
   const __nv_bfloat16* ks = reinterpret_cast<const __nv_bfloat16*>(kvbuf);
   const __nv_bfloat16* vs = ks + kPage * kHeadDim;
-  for (int t = tid; t < Gq * kHalf; t += kMkConsumers) {
-    const int j = t / kHalf, i = t % kHalf;
+  for (int t = tid; t < (jh - jl) * kHalf; t += kMkConsumers) {
+    const int j = jl + t / kHalf, i = t % kHalf;
     const int r0 = (g * Gq + j) * kHeadDim + i;
     const float v0 = mk_qkv_val(p, bias, tab, r0), v1 = mk_qkv_val(p, bias, tab, r0 + kHalf);
     const float cs = p.rope[((size_t)pos * kHalf + i) * 2], sn = p.rope[((size_t)pos * kHalf + i) * 2 + 1];
@@ -447,15 +450,17 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
       const float sn = p.rope[((size_t)pos * kHalf + tid) * 2 + 1];
       const __nv_bfloat16 y0 = __float2bfloat16_rn(v0 * cs - v1 * sn);
       const __nv_bfloat16 y1 = __float2bfloat16_rn(v1 * cs + v0 * sn);
-      p.k_pool[base + tid] = y0;
-      p.k_pool[base + tid + kHalf] = y1;
+      if (hp == 0) {  // one head part appends the new position
+        p.k_pool[base + tid] = y0;
+        p.k_pool[base + tid + kHalf] = y1;
+      }
       kn[tid] = bf_to_f(y0);
       kn[tid + kHalf] = bf_to_f(y1);
     } else if (tid < kHalf + kHeadDim) {
       const int d2 = tid - kHalf;
       const int r = p.q_dim + p.kv_dim + g * kHeadDim + d2;
       const __nv_bfloat16 y = __float2bfloat16_rn(mk_qkv_val(p, bias, tab, r));
-      p.v_pool[base + d2] = y;
+      if (hp == 0) p.v_pool[base + d2] = y;
       vn[d2] = bf_to_f(y);
     }
   }
@@ -501,7 +506,7 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
         }
 #pragma unroll
         for (int j = 0; j < kMkMaxGq; ++j) {
-          if (j < Gq) {
+          if (j >= jl && j < jh) {
             float a = 0.f;
 #pragma unroll
             for (int e4 = 0; e4 < 4; ++e4) {
@@ -517,7 +522,7 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
       }
 #pragma unroll
       for (int j = 0; j < kMkMaxGq; ++j) {
-        if (j < Gq) {
+        if (j >= jl && j < jh) {
           float a = sc[j];
           a += __shfl_xor_sync(0xffffffffu, a, 1);
           a += __shfl_xor_sync(0xffffffffu, a, 2);
@@ -528,7 +533,7 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
     }
     cbar();
     SUB_EV();  // scores
-    if (warp < Gq) {  // online softmax of head `warp` over this page
+    if (warp >= jl && warp < jh) {  // online softmax of head `warp` over this page
       const int j = warp;
       const float s0 = ps[j * 64 + lane], s1 = ps[j * 64 + lane + 32];
       const float mx = warp_max(fmaxf(s0, s1));
@@ -558,13 +563,13 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
       }
 #pragma unroll
       for (int j = 0; j < kMkMaxGq; ++j)
-        if (j < Gq) acc[j] *= alph[j];
+        if (j >= jl && j < jh) acc[j] *= alph[j];
 #pragma unroll
       for (int q = 0; q < kPPG; ++q)
         if (grp * kPPG + q >= nval) vf[q] = 0.f;  // slots past the context may hold garbage
 #pragma unroll
       for (int j = 0; j < kMkMaxGq; ++j) {
-        if (j < Gq) {
+        if (j >= jl && j < jh) {
 #pragma unroll
           for (int q4 = 0; q4 < kPPG / 4; ++q4) {
             const float4 pp = *reinterpret_cast<const float4*>(ps + j * 64 + grp * kPPG + q4 * 4);
@@ -615,6 +620,7 @@ SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, float* sm) {
     for (int q = grp; q < S_a; q += kMkWarps) {
       const float* a = p.apart + ((size_t)(g * S_a + q) * kMkMaxGq + j) * 130;
       const float ms = __ldcg(a + 128), ls = __ldcg(a + 129), os = __ldcg(a + d);
+      if (ms == -INFINITY) continue;  // a head-split CTA's slot for a head it does not own
       const float mn = fmaxf(m, ms);
       const float x = exp2f(m - mn), y = exp2f(ms - mn);
       l = l * x + ls * y;
@@ -695,7 +701,7 @@ SR_DEV void l2_prefetch(const void* ptr, uint32_t bytes) {
 // pages, pulled into L2 a layer early: under the weight stream an HBM miss
 // costs several microseconds on the latency-bound path (l == L: next token).
 SR_DEV void mk_prefetch_next_layer(const MkParams& p, int l, int pos, const int* page_table,
-                                   int c, int G, int S_a, int npages) {
+                                   int c, int G, int S_a, int hs, int npages) {
   if (l >= p.L) {  // layer 0 of the next token: its RoPE row too
     l = 0;
     ++pos;
@@ -707,9 +713,9 @@ SR_DEV void mk_prefetch_next_layer(const MkParams& p, int l, int pos, const int*
     l2_prefetch(ly.ln2, p.d * 2);
     l2_prefetch(ly.bqkv, p.qkv_rows * 2);
   }
-  const int g = c / S_a, s = c % S_a;
-  if (g >= p.KV) return;
-  const int p0 = (int)((long long)npages * s / S_a), p1 = (int)((long long)npages * (s + 1) / S_a);
+  const int g = c / S_a, s = (c % S_a) / hs, PS = S_a / hs;
+  if (g >= p.KV || (c % S_a) % hs != 0) return;  // one head part prefetches the pages
+  const int p0 = (int)((long long)npages * s / PS), p1 = (int)((long long)npages * (s + 1) / PS);
   for (int pg = p0; pg < p1; ++pg) {
     const size_t off = kv_offset(l, page_table[pg], g, 0, p.n_pages, p.KV);
     l2_prefetch(p.k_pool + off, kPage * kHeadDim * 2);
@@ -855,6 +861,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
     int S_a = G / p.KV;
     if (S_a > (npages + p.min_pages - 1) / p.min_pages) S_a = (npages + p.min_pages - 1) / p.min_pages;
     if (S_a < 1) S_a = 1;
+    // more CTAs than page splits (short contexts): split each page's query
+    // heads over hs CTAs too, so idle CTAs share the per-page latency chain
+    int hs = p.head_split ? (G / p.KV) / S_a : 1;
+    if (hs > p.H / p.KV) hs = p.H / p.KV;
+    if (hs < 1) hs = 1;
+    S_a *= hs;
     Top2 best;
     best.init();
     for (int l = 0; l < L; ++l) {
@@ -871,14 +883,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       MK_EV();  // 3 sync
       // attention (+ merge of the splits by the last split CTA of each kv head)
       const uint64_t ta0 = global_ns();
-      mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, npages, scratch, kvbuf,
+      mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, hs, npages, scratch, kvbuf,
                    &kvbar, kvpar);
       if (p.prof && threadIdx.x == 0 && l == 1 && tstep < 40) {  // per-CTA attention time, layer 1
         p.prof[1280 + c] = global_ns() - ta0;
         p.prof[1440 + c] = (c % S_a) == S_a - 1;
       }
       // warm L2 with what the next layer reads on its latency-bound path
-      if (threadIdx.x == 0) mk_prefetch_next_layer(p, l + 1, pos, page_table, c, G, S_a, npages);
+      if (threadIdx.x == 0)
+        mk_prefetch_next_layer(p, l + 1, pos, page_table, c, G, S_a, hs, npages);
       MK_EV();  // 4 attention
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 5 sync
