@@ -607,7 +607,7 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
 // COMBINE: merge the attention splits.  Work item = (query head, 32-dim slice),
 // spread over the grid; 16 thread groups each take every 16th split, one
 // round trip of loads, then a fixed-order merge of the groups (deterministic).
-SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, float* sm) {
+SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, int hs, float* sm) {
   const int Gq = p.H / p.KV;
   const int tid = threadIdx.x, dl = tid & 31, grp = tid >> 5;
   float* r_o = sm;               // [16][32]
@@ -616,8 +616,11 @@ SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, float* sm) {
   for (int it = c; it < p.H * 4; it += G) {
     const int h = it >> 2, d = (it & 3) * 32 + dl;
     const int g = h / Gq, j = h - g * Gq;
+    // with head splits only the part owning head j holds data: splits s*hs + hp
+    int hp = 0;
+    while (hp + 1 < hs && Gq * (hp + 1) / hs <= j) ++hp;
     float m = -INFINITY, l = 0.f, o = 0.f;
-    for (int q = grp; q < S_a; q += kMkWarps) {
+    for (int q = grp * hs + hp; q < S_a; q += kMkWarps * hs) {
       const float* a = p.apart + ((size_t)(g * S_a + q) * kMkMaxGq + j) * 130;
       const float ms = __ldcg(a + 128), ls = __ldcg(a + 129), os = __ldcg(a + d);
       if (ms == -INFINITY) continue;  // a head-split CTA's slot for a head it does not own
@@ -895,7 +898,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       MK_EV();  // 4 attention
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 5 sync
-      mk_combine(p, c, G, S_a, scratch);
+      mk_combine(p, c, G, S_a, hs, scratch);
       MK_EV();  // 6 combine
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 7 sync
