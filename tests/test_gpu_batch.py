@@ -69,12 +69,13 @@ def test_generate_batch_matches_single(tiny):
             assert margins[first] < TOL, (k, first, margins[first])
 
 
-def test_score_batch_fullwidth_7b_vs_oracle(cuda):
-    """Real 7B widths (2 layers): 8 verify-sized sequences in one pass, each
-    readout against the fp32 oracle."""
+@pytest.mark.parametrize("model", ["qwen2.5-7b", "qwq-32b"])
+def test_score_batch_fullwidth_vs_oracle(cuda, model):
+    """Real 7B / 32B widths (2 layers): 8 verify-sized sequences in one pass,
+    each readout against the fp32 oracle."""
     from paper_2504_07891_b200.backend import B200Backend
 
-    full = get_spec("qwen2.5-7b")
+    full = get_spec(model)
     spec = dataclasses.replace(full, n_layers=2)
     w = make_weights(full, 0, layers=[0, 1])
     v = shared_vocab(spec.vocab_text)
