@@ -307,6 +307,10 @@ def run_ours(args) -> None:
                      "draft_decode_GBps": round(ds.decode_bytes / (ds.decode_ms * 1e-3) / 1e9, 1)
                      if ds.decode_ms > 0 else None},
         "gpu_launches": ds.launches + db.launches,
+        **({"batching": {"trajectories_in_flight": args.batch,
+                         "device_passes": len(sched.batches),
+                         "mean_requests_per_pass": round(sum(sched.batches) / max(1, len(sched.batches)), 2)}}
+           if sched is not None else {}),
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
