@@ -150,7 +150,7 @@ class BatchScheduler:
             groups.setdefault(id(it[0]), []).append(it)
         for chunk_all in groups.values():
             backend = chunk_all[0][0]
-            cap = len(backend.pool.streams)
+            cap = max(1, len(backend.pool.streams) - len(backend.pool.busy))  # free KV streams
             for i in range(0, len(chunk_all), cap):
                 chunk = chunk_all[i:i + cap]
                 reqs = [it[2] for it in chunk]
@@ -169,7 +169,7 @@ class BatchScheduler:
         deferred = []
         for backend, kind, req, fut in items:
             _, gens = live.setdefault(id(backend), (backend, []))
-            if len(gens) >= len(backend.pool.streams):
+            if len(backend.pool.busy) >= len(backend.pool.streams) - 1:  # keep one for scoring
                 deferred.append((backend, kind, req, fut))
                 continue
             try:
@@ -199,6 +199,7 @@ class BatchScheduler:
             if isinstance(exc, RuntimeError) and type(exc).__name__ == "NativeError":
                 err = backend._device_error(exc)
             for g in gens:
+                backend.gen_release(g)
                 g["fut"].set_result(err)
             gens.clear()
             return
@@ -227,6 +228,7 @@ class BatchScheduler:
             err = exc
             if isinstance(exc, RuntimeError) and type(exc).__name__ == "NativeError":
                 err = backend._device_error(exc)
+            backend.gen_release(g)
             g["fut"].set_result(err)
             gens.clear()
             return

@@ -117,17 +117,22 @@ class StreamPool:
     def __init__(self, n: int) -> None:
         self.streams = [Stream(i) for i in range(n)]
         self._clock = 0
+        # streams held by open (continuously batched) generations: never handed out
+        self.busy: set = set()
 
     def acquire(self, ids: Sequence[int], exclude=()) -> tuple[Stream, int]:
         best, best_len = None, -1
         for s in self.streams:
-            if s in exclude:
+            if s in exclude or s in self.busy:
                 continue
             l = common_prefix(s.ids, ids)
             if l > best_len or (l == best_len and best is not None and s.stamp > best.stamp):
                 best, best_len = s, l
         if best_len == 0:
-            best = min((s for s in self.streams if s not in exclude), key=lambda s: s.stamp)
+            free = [s for s in self.streams if s not in exclude and s not in self.busy]
+            if not free:
+                raise RuntimeError("every KV stream of this backend is in use")
+            best = min(free, key=lambda s: s.stamp)
         self._clock += 1
         best.stamp = self._clock
         # at least one prompt token is always recomputed: its logits seed decode
@@ -295,7 +300,7 @@ class ModelBackend(Backend):
 
     # -- several requests in one device pass -----------------
     def _acquire_many(self, id_lists):
-        if len(id_lists) > len(self.pool.streams):
+        if len(id_lists) > len(self.pool.streams) - len(self.pool.busy):
             raise ValueError(f"{len(id_lists)} requests need as many KV streams "
                              f"(this backend has {len(self.pool.streams)})")
         chosen, keeps = [], []
@@ -331,6 +336,7 @@ class ModelBackend(Backend):
         ids = self._prompts.encode(request.prompt)
         stream, keep = self.pool.acquire(ids, exclude=exclude)
         self.engine.truncate(stream, keep)
+        self.pool.busy.add(stream)
         n_rows = getattr(self.engine, "n_ids", None) or self.engine.spec.vocab_rows
         return {"stream": stream, "feed": ids[keep:], "gen": [], "max": request.max_tokens,
                 "stop": tuple(request.stop),
@@ -341,7 +347,11 @@ class ModelBackend(Backend):
         return (g["gen"] and g["classes"][g["gen"][-1]] in (CLASS_STOP, CLASS_END_THINK)) \
             or len(g["gen"]) >= g["max"]
 
+    def gen_release(self, g: dict) -> None:
+        self.pool.busy.discard(g["stream"])
+
     def gen_close(self, g: dict):
+        self.gen_release(g)
         T = self.types
         gen = g["gen"]
         finish = finish_of(gen, g["classes"])

@@ -62,3 +62,21 @@ def test_reference_run_sweep_through_scheduler(stepspec, tmp_path):
         sched.close()
     assert len(res.records) == 3
     assert max(sched.batches) > 1
+
+
+def test_open_generation_streams_are_not_reused():
+    """A stream held by a continuously batched generation is never handed to
+    another request, even when it is the least recently used one."""
+    small = oracle_backend("tiny-draft", BackendRole.SMALL, n_streams=3)
+    v = shared_vocab(small.engine.spec.vocab_text)
+    from paper_2504_07891_b200.contract import GenerationRequest
+    from paper_2504_07891_b200.domain import render_generation_prompt
+
+    g = small.gen_open(GenerationRequest(prompt=render_generation_prompt(v.problem(16, 1), ""),
+                                         max_tokens=4))
+    held = g["stream"]
+    for k in range(6):  # unrelated prompts cycle through the other streams
+        st, _ = small.pool.acquire(v.encode(render_generation_prompt(v.problem(16, 50 + k), "")))
+        assert st is not held
+    small.gen_release(g)
+    assert held not in small.pool.busy
