@@ -234,8 +234,9 @@ class NativeEngine:
         free = self.model.free_pages
         while len(pg.pages) < need:
             if not free:
-                victims = sorted((s for s in self.streams
-                                  if s is not stream and s not in protect and s.handle.pages),
+                busy = getattr(self, "busy", ())
+                victims = sorted((s for s in self.streams if s is not stream and s not in protect
+                                  and s not in busy and s.handle.pages),
                                  key=lambda s: s.stamp)
                 if not victims:
                     raise MemoryError("K/V page pool exhausted")

@@ -204,6 +204,7 @@ class ModelBackend(Backend):
         self.types = types or own_types()
         self.threshold = threshold
         self.pool = StreamPool(n_streams)
+        self.engine.busy = self.pool.busy  # never evicted for another stream
         for s in self.pool.streams:
             engine.attach(s)
         self._lock = threading.Lock()
