@@ -19,6 +19,7 @@ would have produced alone.
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from concurrent.futures import Future
@@ -140,9 +141,10 @@ class BatchScheduler:
             if deferred:
                 with self._cv:
                     self._pending = deferred + self._pending
+            busy_backends = sum(1 for _, gs in live.values() if gs)
             for backend, gens in live.values():
                 if gens:
-                    self._step(backend, gens)
+                    self._step(backend, gens, shared=busy_backends > 1)
 
     def _scores(self, items) -> None:
         groups: dict[int, list] = {}
@@ -183,12 +185,15 @@ class BatchScheduler:
         return deferred
 
     # a lone generation runs `solo_tokens` at a time on the single-stream
-    # decode path (the persistent kernel) instead of one-token batched passes
+    # decode path (the persistent kernel) instead of one-token batched passes;
+    # `solo_tokens_shared` when the other backend has live generations too, so
+    # a long base chunk does not stall the drafts
     solo_tokens = 16
+    solo_tokens_shared = int(os.environ.get("SR_SOLO_SHARED", "4"))
 
-    def _step(self, backend, gens: list) -> None:
+    def _step(self, backend, gens: list, shared: bool = False) -> None:
         if len(gens) == 1 and hasattr(backend.engine, "generate"):
-            return self._solo(backend, gens)
+            return self._solo(backend, gens, self.solo_tokens_shared if shared else self.solo_tokens)
         try:
             with backend._lock:
                 toks = backend.engine.step_batch([g["stream"] for g in gens],
@@ -217,9 +222,9 @@ class BatchScheduler:
                 keep.append(g)
         gens[:] = keep
 
-    def _solo(self, backend, gens: list) -> None:
+    def _solo(self, backend, gens: list, chunk: int) -> None:
         g = gens[0]
-        n = min(self.solo_tokens, g["max"] - len(g["gen"]))
+        n = min(chunk, g["max"] - len(g["gen"]))
         try:
             with backend._lock:
                 # stop ids end the chunk exactly as they end a generation
