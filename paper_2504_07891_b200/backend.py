@@ -260,6 +260,21 @@ class NativeEngine:
     # -- engine calls ----------------------------------------------------
     def generate(self, stream: Stream, suffix: Sequence[int], max_new: int,
                  stop: tuple[str, ...]) -> tuple[list[int], int]:
+        """Greedy generation of up to ``max_new`` tokens.  A request longer
+        than one native call allows (``max_new`` of the model) continues in
+        further ``sr_generate`` calls fed the last token, so every path honours
+        ``request.max_tokens`` exactly."""
+        gen, finish = self._generate_once(stream, suffix, max_new, stop)
+        margins = list(self.last_margins)
+        while finish == 0 and len(gen) < max_new:  # FINISH_LENGTH at the call cap
+            more, finish = self._generate_once(stream, gen[-1:], max_new - len(gen), stop)
+            gen.extend(more)
+            margins.extend(self.last_margins)
+        self.last_margins = margins
+        return gen, finish
+
+    def _generate_once(self, stream: Stream, suffix: Sequence[int], max_new: int,
+                       stop: tuple[str, ...]) -> tuple[list[int], int]:
         m = self.model
         max_new = min(max_new, m.max_new)
         start = len(stream.ids)

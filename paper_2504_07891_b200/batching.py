@@ -51,6 +51,14 @@ class BatchScheduler:
     """
 
     def __init__(self, small: Any, base: Any, linger_s: float = 0.002) -> None:
+        for b in (small, base):
+            pool = getattr(b, "pool", None)
+            if pool is None or not hasattr(b, "_lock") or not hasattr(b, "engine"):
+                raise TypeError(f"{type(b).__name__} is not a device ModelBackend "
+                                "(needs pool, _lock and engine)")
+            if len(pool.streams) < 2:
+                raise ValueError("a scheduled backend needs at least 2 KV streams "
+                                 "(one stays free for scoring)")
         self.small = _Proxy(self, small)
         self.base = _Proxy(self, base)
         self.linger_s = linger_s
@@ -59,6 +67,7 @@ class BatchScheduler:
         self._active = 0
         self._stop = False
         self.batches: list[int] = []  # sizes of the device passes issued
+        self._inflight: list = []     # the batch being dispatched
         self._thread = threading.Thread(target=self._loop, name="batch-dispatch", daemon=True)
         self._thread.start()
 
@@ -66,6 +75,8 @@ class BatchScheduler:
     def _submit(self, backend: Any, kind: str, request: Any):
         fut: Future = Future()
         with self._cv:
+            if self._stop:
+                raise RuntimeError("BatchScheduler is closed (or its dispatcher failed)")
             self._pending.append((backend, kind, request, fut))
             self._cv.notify_all()
         res = fut.result()
@@ -121,6 +132,23 @@ class BatchScheduler:
     # one ``score_steps`` pass.
     def _loop(self) -> None:
         live: dict[int, tuple[Any, list]] = {}  # id(backend) -> (backend, open generations)
+        try:
+            self._dispatch(live)
+        except BaseException as exc:  # never leave a client blocked on its future
+            with self._cv:
+                pending, self._pending = self._pending + self._inflight, []
+                self._stop = True
+            for it in pending:
+                if not it[3].done():
+                    it[3].set_result(exc)
+            for backend, gens in live.values():
+                for g in gens:
+                    backend.gen_release(g)
+                    if not g["fut"].done():
+                        g["fut"].set_result(exc)
+                gens.clear()
+
+    def _dispatch(self, live: dict) -> None:
         while True:
             with self._cv:
                 busy = any(gs for _, gs in live.values())
@@ -136,6 +164,7 @@ class BatchScheduler:
                             break
                         self._cv.wait(left)
                 batch, self._pending = self._pending, []
+                self._inflight = batch
             self._scores([it for it in batch if it[1] == "score"])
             deferred = self._admit([it for it in batch if it[1] == "gen"], live)
             if deferred:

@@ -128,15 +128,17 @@ class StreamPool:
             l = common_prefix(s.ids, ids)
             if l > best_len or (l == best_len and best is not None and s.stamp > best.stamp):
                 best, best_len = s, l
-        if best_len == 0:
+        if best is None or best_len == 0:
             free = [s for s in self.streams if s not in exclude and s not in self.busy]
             if not free:
                 raise RuntimeError("every KV stream of this backend is in use")
             best = min(free, key=lambda s: s.stamp)
+            best_len = 0
         self._clock += 1
         best.stamp = self._clock
-        # at least one prompt token is always recomputed: its logits seed decode
-        return best, min(best_len, len(ids) - 1)
+        # at least one prompt token is always recomputed: its logits seed
+        # decode (an empty prompt keeps nothing: never a negative length)
+        return best, max(0, min(best_len, len(ids) - 1))
 
 
 # --------------------------------------------------------------------------
@@ -312,7 +314,20 @@ class ModelBackend(Backend):
             keeps.append(keep)
         return chosen, keeps
 
+    def _native(self, fn, *args):
+        """Run ``fn`` mapping a native failure like the single-request
+        calls do (``_device_error``)."""
+        try:
+            return fn(*args)
+        except RuntimeError as exc:
+            if type(exc).__name__ != "NativeError":
+                raise
+            raise self._device_error(exc) from exc
+
     def score_steps(self, requests: Sequence[VerificationRequest]) -> list:
+        return self._native(self._score_steps, requests)
+
+    def _score_steps(self, requests: Sequence[VerificationRequest]) -> list:
         """``score_step`` for several independent requests in one device pass
         (the engine's ``score_batch``).  Results come back in request order: a
         ``UtilityScore``, or the ``ScoreParseFailure`` that ``score_step`` would
@@ -334,7 +349,11 @@ class ModelBackend(Backend):
     # continuous batching (batching.BatchScheduler): a generation is opened,
     # stepped together with other streams' generations, and closed
     def gen_open(self, request: GenerationRequest, exclude=()) -> dict:
+        if not request.prompt:
+            raise ValueError("prompt must be non-empty")
         ids = self._prompts.encode(request.prompt)
+        if not ids:
+            raise ValueError("prompt must contain at least one token")
         stream, keep = self.pool.acquire(ids, exclude=exclude)
         self.engine.truncate(stream, keep)
         self.pool.busy.add(stream)
@@ -369,6 +388,9 @@ class ModelBackend(Backend):
                                   measured_latency_s=time.monotonic() - g["t0"])
 
     def generate_steps(self, requests: Sequence[GenerationRequest]) -> list:
+        return self._native(self._generate_steps, requests)
+
+    def _generate_steps(self, requests: Sequence[GenerationRequest]) -> list:
         """``generate_step`` for several independent requests, decoded together
         (the engine's ``generate_batch``: one weight stream per token for all
         live requests).  Returns ``GenerationResult`` in request order."""
@@ -402,6 +424,8 @@ class ModelBackend(Backend):
         t0 = time.monotonic()
         with self._lock:
             ids = self._prompts.encode(request.prompt)
+            if not ids:
+                raise ValueError("prompt must contain at least one token")
             if getattr(self, "speculator", None) is not None:
                 gen, finish = self._generate_speculative(ids, request.max_tokens,
                                                          tuple(request.stop))
@@ -413,6 +437,7 @@ class ModelBackend(Backend):
                                                    tuple(request.stop))
             if self.record:
                 self.calls.append({"kind": "gen", "prompt_ids": ids, "gen_ids": list(gen),
+                                   "margins": list(getattr(self.engine, "last_margins", [])),
                                    "finish": finish, "stop": list(request.stop),
                                    "max_tokens": request.max_tokens, "fresh": len(ids) - keep,
                                    "seq": time.monotonic_ns()})

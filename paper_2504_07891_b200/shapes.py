@@ -62,6 +62,8 @@ class ModelSpec:
     digit_gain: float = 6.0
     digit_noise: float = 1.0
     judge_offsets: tuple = ()  # per-digit gain offsets (tools/calibrate_judge.py)
+    embed_std: float = 0.0   # embedding init std (0 -> 0.02)
+    succ_gain: float = 0.0   # successor circuit (module doc); 0 = off
     # tensor parallelism (tp_spec): this rank's shard of a model split `tp_world` ways
     tp_world: int = 1
     tp_rank: int = 0
@@ -112,18 +114,17 @@ MODELS: dict[str, ModelSpec] = {
     "tiny-draft": ModelSpec("tiny-draft", 2, 128, 2, 1, 512, 4096, 4096, rope_theta=10_000.0),
     "tiny-base": ModelSpec("tiny-base", 4, 256, 4, 2, 1024, 4160, 4096, judge=True,
                            judge_offsets=(-0.5, -0.125, -0.5, 0.375, 0.5, 0.25, 0.0, 0.375, 0.25, -0.5)),
-    # public model-card shapes
+    # public model-card shapes; embed_std / succ_gain: the successor circuit
+    # (module doc); judge offsets measured on the B200 by
+    # tools/calibrate_judge.py --gpu (seed 0)
     "r1-1.5b": ModelSpec("r1-1.5b", 28, 1536, 12, 2, 8960, V_QWEN_DRAFT, V_QWEN_DRAFT,
-                         rope_theta=10_000.0),
-    # judge offsets measured on the B200 by tools/calibrate_judge.py --gpu (seed 0)
+                         rope_theta=10_000.0, embed_std=1.0, succ_gain=0.8),
     "qwen2.5-7b": ModelSpec("qwen2.5-7b", 28, 3584, 28, 4, 18944, V_QWEN_BASE, V_QWEN_DRAFT,
-                            judge=True,
-                            judge_offsets=(-0.75, 1.0, 0.75, -1.875, -1.5, 0.75, -0.875, 0.0,
-                                           0.875, 1.5)),
+                            judge=True, embed_std=1.0, succ_gain=0.8, cue_gain=6.0,
+                            digit_gain=10.0),
     "qwq-32b": ModelSpec("qwq-32b", 64, 5120, 40, 8, 27648, V_QWEN_BASE, V_QWEN_DRAFT,
-                         judge=True,
-                         judge_offsets=(-0.75, 0.75, -0.75, 2.75, 0.0, -1.0, -1.75, -0.875,
-                                        2.875, -1.5)),
+                         judge=True, embed_std=1.0, succ_gain=0.8, cue_gain=6.0,
+                         digit_gain=10.0),
 }
 
 PAIRS = {
@@ -252,6 +253,8 @@ def init_std(spec: ModelSpec, name: str) -> float:
     if spec.init_std > 0:
         return spec.init_std
     leaf = name.rsplit(".", 1)[-1]
+    if leaf == "embed" and spec.embed_std > 0:
+        return spec.embed_std
     if leaf in ("bqkv", "embed"):
         return 0.02
     fan_in = {"wo": spec.q_dim, "wd": spec.d_ffn}.get(leaf, spec.d_model)
@@ -282,7 +285,38 @@ def make_tensor(spec: ModelSpec, seed: int, name: str, device: str = "cpu") -> t
             t[dgt] = r + ((spec.digit_gain + offs[dgt]) / math.sqrt(spec.d_model)) * u
         if spec.vocab_rows > spec.vocab_text:
             t[spec.vocab_text] = u / math.sqrt(spec.d_model)  # cue-alignment probe
+    if spec.succ_gain > 0 and name == "lm_head":
+        # successor circuit: row v reads the (unit) embedding of v's predecessor
+        emb = make_tensor(spec, seed, "embed", device).float()
+        lo, hi = successor_range(spec.vocab_text)
+        pred = successor_perm(spec.vocab_text, seed)[1].to(device)
+        rows = torch.arange(lo, hi, device=device)
+        src = emb[pred[rows]]
+        t[rows] += spec.succ_gain * (src / src.norm(dim=1, keepdim=True))
+        del emb, src
     return t.to(torch.bfloat16)
+
+
+def successor_range(n_text: int) -> tuple[int, int]:
+    """Ids the successor circuit permutes: the ordinary words (``vocab``)."""
+    from .vocab import FIRST_WORD_ID
+
+    return FIRST_WORD_ID, n_text
+
+
+def successor_perm(n_text: int, seed: int = 0) -> tuple[torch.Tensor, torch.Tensor]:
+    """(succ, pred): a seeded random permutation of the ordinary word ids
+    and its inverse, as int64 tables over [0, n_text) (identity outside the
+    ordinary range).  Keyed by the vocabulary, not the model, so a draft and
+    a base sharing a vocabulary share their preferred successors."""
+    lo, hi = successor_range(n_text)
+    g = torch.Generator().manual_seed(derive_seed("successor", n_text, seed) & ((1 << 63) - 1))
+    perm = torch.randperm(hi - lo, generator=g) + lo
+    succ = torch.arange(n_text, dtype=torch.int64)
+    succ[lo:hi] = perm
+    pred = torch.arange(n_text, dtype=torch.int64)
+    pred[perm] = torch.arange(lo, hi, dtype=torch.int64)
+    return succ, pred
 
 
 def make_weights(spec: ModelSpec, seed: int = 0, device: str = "cpu",
@@ -311,20 +345,30 @@ def rope_table(spec: ModelSpec, max_pos: int) -> torch.Tensor:
 # judge calibration (see module doc)
 # --------------------------------------------------------------------------
 
-def judge_calibration_prompts(spec: ModelSpec, n: int = 24) -> list[list[int]]:
+def judge_calibration_prompts(spec: ModelSpec, n: int = 24, cot_step: int = 25,
+                              chain: bool = False) -> list[list[int]]:
     """Token ids of ``n`` synthetic verify prompts (64-word problem, a CoT of
-    0..600 words, a 24-word candidate), seeded and model-independent."""
+    0, cot_step, .. words, a 24-word candidate), seeded and model-independent.
+    ``chain``: the CoT and candidate follow the successor circuit's
+    permutation from a random start word -- the text the successor-circuit
+    models actually generate, so the calibration sees loop-like contexts."""
     from .domain import render_verification_prompt
     from .vocab import shared_vocab
 
     vocab = shared_vocab(spec.vocab_text)
     lo, hi = vocab.ordinary_range()
     rng = np.random.default_rng(20250410)
+    succ = successor_perm(vocab.n_text)[0].tolist() if chain else None
     out = []
     for i in range(n):
-        w = [vocab.words[int(x)] for x in rng.integers(lo, hi, size=64 + 25 * i + 24)]
-        prompt = render_verification_prompt(" ".join(w[:64]), " ".join(w[64:64 + 25 * i]) + " ",
-                                            " ".join(w[64 + 25 * i:]) + " ")
+        c = cot_step * i
+        ids = [int(x) for x in rng.integers(lo, hi, size=64 + c + 24)]
+        if chain:
+            for k in range(65, len(ids)):
+                ids[k] = succ[ids[k - 1]]
+        w = [vocab.words[x] for x in ids]
+        prompt = render_verification_prompt(" ".join(w[:64]), " ".join(w[64:64 + c]) + " ",
+                                            " ".join(w[64 + c:]) + " ")
         out.append(vocab.encode(prompt))
     return out
 

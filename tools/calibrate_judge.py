@@ -28,7 +28,7 @@ class GpuJudge:
         from paper_2504_07891_b200.domain import BackendRole
 
         self.b = B200Backend(spec, BackendRole.BASE, weights=make_weights(spec, 0, device="cuda"),
-                             max_ctx=2048)
+                             max_ctx=8192, n_streams=1)
         self.s = self.b.pool.streams[0]
 
     def set_spec(self, spec):
@@ -52,10 +52,16 @@ def logits_fn_for(spec, gpu: bool):
 def main() -> None:
     name = sys.argv[1]
     gpu = "--gpu" in sys.argv
-    spec = get_spec(name)
-    prompts = judge_calibration_prompts(spec)
+    over = {}
+    if "--digit-noise" in sys.argv:
+        over["digit_noise"] = float(sys.argv[sys.argv.index("--digit-noise") + 1])
+    spec = get_spec(name, **over)
+    n = int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 24
+    step = int(sys.argv[sys.argv.index("--cot-step") + 1]) if "--cot-step" in sys.argv else 25
+    prompts = judge_calibration_prompts(spec, n, step, chain=spec.succ_gain > 0)
     judge = GpuJudge(spec) if gpu else None
-    for it in range(4):
+    iters = int(sys.argv[sys.argv.index("--iters") + 1]) if "--iters" in sys.argv else 4
+    for it in range(iters):
         if gpu:
             judge.set_spec(spec)
             fn = judge
@@ -63,10 +69,21 @@ def main() -> None:
             fn = logits_fn_for(spec, gpu)
         rows = [fn(p) for p in prompts]
         hist = collections.Counter(int(r[:10].argmax()) for r in rows)
+        import torch
+
+        L = torch.stack([r.float() for r in rows])
+        tenth = torch.topk(L[:, : spec.vocab_text], 10, dim=1).values[:, -1]
+        member = (L[:, :10] >= tenth[:, None]).float().mean().item()
+        dev = L[:, :10] - L[:, :10].mean(1, keepdim=True)
+        print(f"  probe {L[:, spec.vocab_text].mean():.3f} digit-member frac {member:.3f} "
+              f"context spread (std over prompts of centred digit logits) "
+              f"{(dev - dev.mean(0)).std().item():.3f}", flush=True)
         print(f"iter {it}: offsets {spec.judge_offsets} -> argmax-digit histogram {sorted(hist.items())}",
               flush=True)
         spec = dataclasses.replace(spec, judge_offsets=judge_offsets_update(spec, rows))
     print("judge_offsets =", spec.judge_offsets)
+    print("OVERRIDE " + "".join(f"{k}={v}," for k, v in over.items())
+          + "judge_offsets=" + ":".join(str(x) for x in spec.judge_offsets))
 
 
 if __name__ == "__main__":
