@@ -1,29 +1,39 @@
 """SpecReason inner-loop benchmark (BASELINE.json metric: CoT tokens/s and ms
 per reasoning step, draft + verify + fallback).
 
-One *step* is one iteration of the SpecReason thinking loop driven through the
+Workload (default, N=1): configuration C3 -- R1-Distill-1.5B-shape draft +
+QwQ-32B-shape base, random-init bf16 (seeded, with the documented successor /
+judge weight circuits of ``shapes.py``), greedy, threshold 7, 8192-token
+thinking budget, 64-word synthetic problems (``dp.problem_text``).  One
+*step* is one iteration of the SpecReason thinking loop driven through the
 public API (``driver.SpecReasonSession`` over two ``B200Backend``s): the draft
 decodes a step, the base scores it in one prefill pass, and on reject the base
-regenerates it.  Steps are taken in order from back-to-back configuration-C2
-trajectories (1.5B-shape draft + 7B-shape base, random-init bf16, greedy,
-threshold 7, 4096-token thinking budget, 64-token synthetic problems); a new
-trajectory (new problem) starts whenever one ends.
+regenerates it.  The timed window is mid-trajectory: an untimed fast-forward
+runs the trajectory to half its thinking budget (4096 CoT tokens, so the
+timed steps see the trajectory's mean context), then W warm-up steps, then
+the K timed steps.
 
 Reported (one JSON line, rank 0):
   value      CoT tokens / s over the K timed steps, device time (sum of the
-             CUDA-event durations of every native call: prefill + decode graph
-             + readout), whole job = all ranks' tokens / max rank time
+             CUDA-event durations of every native call: prefill + decode +
+             readout), whole job = all ranks' tokens / max rank time
   e2e        the same metric end to end: wall time of the K steps through the
              public API (tokenisation, the Python driver, H2D of ids, D2H of
-             results), timed with CUDA events + synchronize around the region
-  roofline   the base model's fallback decode step graph (the dominant cost):
-             algorithmic bytes (weights + KV read per token) / its
-             CUDA-event time, against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline  the CPU oracle (fp32, torch on the host cores) on a bounded
-             sample, layer-sliced and extrapolated by weight bytes
-Multi-GPU: one process per GPU (torchrun), independent problems per rank (no
-collective on the data path): scaling "weak".
-``--impl reference`` times the reference loop on the host CPU instead (rank 0).
+             results), CUDA events + synchronize around the region
+  roofline   the kernel instance with the largest device time in the window
+             (draft decode, base decode, or base prefill = verify + fallback
+             prompts): algorithmic bytes / flops (shapes.py) over
+             its CUDA-event time, against MEASURED_PEAKS.json; ``kernels``
+             lists every instance
+  cpu_baseline  the oracle's arithmetic for the first timed steps' recorded
+             calls (full shapes, full depth, real context lengths) executed on
+             the host cores (``oracle/cpu_replay.py``), >= ~20 s of CPU work
+Multi-GPU (torchrun): ``--mode dp`` splits a fixed problem set by problem id
+(``dp.partition``; no collective on the data path, scaling "weak");
+``--mode tp`` shards the base over the ranks (C4).
+``--impl reference`` runs the unmodified reference engine (``baseline/_ref``)
+over a recorded C3 trajectory of this benchmark (``bench_data/``), pricing
+every warm-up and timed step's calls on the host cores (rank 0).
 """
 
 from __future__ import annotations
@@ -56,8 +66,12 @@ def _peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": d["hbm_gbs"], "src": "measured"}
-    return {"hbm_gbs": 6650.0, "src": "fallback"}
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    # /opt/skills/guides/B200_PROFILING.md fallbacks
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1590.0,
+            "src": "fallback (B200_PROFILING.md)"}
 
 
 class ClockSampler:
@@ -141,24 +155,30 @@ def _reduce_sum(dist, v: float) -> float:
 
 
 class StepSource:
-    """Endless sequence of SpecReason steps over back-to-back trajectories."""
+    """Endless sequence of SpecReason steps over back-to-back trajectories of
+    the problems ``problem_ids`` (``dp.problem_text``)."""
 
-    def __init__(self, small, base, config, problems, vocab) -> None:
+    def __init__(self, small, base, config, problem_ids, vocab) -> None:
         from paper_2504_07891_b200.driver import SpecReasonSession
 
         self.cls = SpecReasonSession
         self.small, self.base, self.config = small, base, config
-        self.problems = problems
+        self.problem_ids = list(problem_ids)
         self.vocab = vocab
         self.k = 0
         self.trajectories = 0
         self.session = None
+        self.problems: list[str] = []
         self._new()
 
     def _new(self) -> None:
-        seed = self.problems[self.k % len(self.problems)]
+        from paper_2504_07891_b200.dp import problem_text
+
+        pid = self.problem_ids[self.k % len(self.problem_ids)]
         self.k += 1
-        self.session = self.cls(self.config, self.vocab.problem(64, seed), self.small, self.base)
+        text = problem_text(self.vocab, pid)
+        self.problems.append(text)
+        self.session = self.cls(self.config, text, self.small, self.base)
         self.trajectories += 1
 
     def step(self):
@@ -168,10 +188,93 @@ class StepSource:
                 return out
             self._new()
 
+    def fast_forward(self, cot_tokens: int) -> int:
+        """Untimed steps until the current trajectory's CoT holds
+        ``cot_tokens`` tokens (the timed window then sits mid-trajectory)."""
+        n = 0
+        while self.session.run.state.thinking_tokens_used < cot_tokens and self.session.thinking:
+            if self.session.step() is None:
+                break
+            n += 1
+        return n
+
+
+# ------------------------------------------------------------- rooflines --
+def kernel_lines(ds, db, names, peaks, sustained: bool) -> list[dict]:
+    """Per kernel instance of the window: device ms, algorithmic work (SURVEY
+    §8d), achieved rate and roofline fraction."""
+    bw = peaks["hbm_gbs"]
+    tf = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"]
+    out = []
+    for who, st, model in (("draft", ds, names[0]), ("base", db, names[1])):
+        if st.decode_ms > 0:
+            gbs = st.decode_bytes / (st.decode_ms * 1e-3) / 1e9
+            out.append({"kernel": f"decode_mk_kernel ({who} {model} greedy decode, persistent)",
+                        "instance": f"{who}_decode", "ms": round(st.decode_ms, 2),
+                        "tokens": st.decode_tokens,
+                        "bytes_per_token": round(st.decode_bytes / max(1, st.decode_tokens)),
+                        "bound": "hbm", "achieved": round(gbs, 1), "peak": bw, "unit": "GB/s",
+                        "frac": round(gbs / bw, 4)})
+        if st.prefill_ms > 0:
+            t = st.prefill_ms * 1e-3
+            hbm_t = st.prefill_bytes / (bw * 1e9)
+            ten_t = st.prefill_flops / (tf * 1e12)
+            if ten_t > hbm_t:
+                ach, peak, unit, bound = st.prefill_flops / t / 1e12, tf, "TFLOP/s", "tensor"
+            else:
+                ach, peak, unit, bound = st.prefill_bytes / t / 1e9, bw, "GB/s", "hbm"
+            out.append({"kernel": f"prefill pass ({who} {model}: gemm_tc_persistent + "
+                                  "attn_prefill_umma + epilogues"
+                                  + (" + readout" if who == "base" else "") + ")",
+                        "instance": f"{who}_prefill", "ms": round(st.prefill_ms, 2),
+                        "rows": st.prefill_tokens, "bytes": round(st.prefill_bytes),
+                        "flops": round(st.prefill_flops), "bound": bound,
+                        "achieved": round(ach, 1), "peak": peak, "unit": unit,
+                        "frac": round(ach / peak, 4),
+                        "tflops": round(st.prefill_flops / t / 1e12, 1)})
+    return out
+
+
+def _traffic(instance: str, model: str):
+    """DRAM bytes per unit from the committed ncu --set full capture of that
+    kernel instance (profiles/r02_ncu_traffic.json), else None."""
+    p = ROOT / "profiles" / "r02_ncu_traffic.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text()).get(f"{instance}:{model}")
+    if not d:
+        return None, None
+    return d["dram_bytes_per_unit"], d["source"]
+
+
+# ------------------------------------------------------------- call trace --
+def call_descriptors(backend, calls, model_key: str) -> list[dict]:
+    """Compact, replayable form of recorded calls: what the engine received
+    (text / count / finish or score) and what the device computed (context
+    start, fresh rows, generated tokens)."""
+    from paper_2504_07891_b200.host import FINISH_END_THINK, FINISH_STOP
+
+    out = []
+    for c in calls:
+        start = len(c["prompt_ids"]) - c["fresh"]
+        d = {"model": model_key, "kind": c["kind"], "prompt_len": len(c["prompt_ids"]),
+             "start": start, "fresh": c["fresh"]}
+        if c["kind"] == "gen":
+            g = c["gen_ids"]
+            fin = {FINISH_END_THINK: "EndThink", FINISH_STOP: "Stop"}.get(c["finish"], "Length")
+            text_ids = g[:-1] if fin == "EndThink" else g
+            d.update(n_gen=len(g), text=backend.vocab.render(text_ids), token_count=len(text_ids),
+                     finish=fin)
+        else:
+            d.update(score=c["score"], n_gen=1)
+        out.append(d)
+    return out
+
 
 def run_ours(args) -> None:
     from paper_2504_07891_b200 import AcceptanceThreshold, EngineConfig
     from paper_2504_07891_b200.backend import build_pair
+    from paper_2504_07891_b200.dp import partition, problem_ids
     from paper_2504_07891_b200.shapes import PAIRS, get_spec
     from paper_2504_07891_b200.vocab import shared_vocab
 
@@ -183,22 +286,29 @@ def run_ours(args) -> None:
 
         base_tp = TensorParallel.from_dist() if dist is not None else TensorParallel.single()
     extra = {"n_streams": 2 * args.batch + 2, "max_tokens": 1024} if args.batch > 1 else {}
+    record = rank == 0 and args.batch == 1
     small, base = build_pair(args.pair, seed=args.seed, max_ctx=args.budget + 512,
-                             threshold=args.threshold, base_tp=base_tp, **extra)
+                             threshold=args.threshold, base_tp=base_tp, record=record, **extra)
     base.verify_template = args.verify_template
     if args.spec_gamma > 0:  # SpecReason+Decode: the draft proposes tokens inside base fallback
         base.attach_speculator(small, gamma=args.spec_gamma)
-    vocab = shared_vocab(get_spec(PAIRS[args.pair][0]).vocab_text)
+    names = PAIRS[args.pair]
+    vocab = shared_vocab(get_spec(names[0]).vocab_text)
     cfg = EngineConfig(threshold=AcceptanceThreshold(args.threshold), temperature=0.0,
                        token_budget=args.budget, max_step_tokens=args.max_step_tokens)
-    # DP: independent problems per rank; TP: every rank drives the same one
-    problems = [(0 if args.mode == "tp" else rank) * 1000 + i for i in range(64)]
+    # DP: this rank's block of a fixed problem set (problem-id partition, C5);
+    # TP: every rank drives the same trajectories
+    ids = problem_ids(args.problems)
+    mine = ids if args.mode == "tp" else partition(ids, rank, world)
+    ff = args.budget // 2 if args.ff_tokens < 0 else args.ff_tokens
     sched = None
+    ff_steps = 0
+    warm_bounds: list = []
     if args.batch > 1:  # B trajectories, each on its own thread, batched device passes
         from paper_2504_07891_b200.batching import BatchScheduler
 
         sched = BatchScheduler(small, base)
-        srcs = [StepSource(sched.small, sched.base, cfg, problems[k::args.batch], vocab)
+        srcs = [StepSource(sched.small, sched.base, cfg, mine[k::args.batch] or mine, vocab)
                 for k in range(args.batch)]
         per = -(-args.steps // args.batch)
 
@@ -213,19 +323,25 @@ def run_ours(args) -> None:
             trajectories = property(lambda self: sum(x.trajectories for x in srcs))
 
         src = _Multi()
+        if ff > 0:
+            sched.run([lambda s_, b_, src=src: src.fast_forward(ff) for src in srcs])
         run_steps(max(1, -(-args.warmup // args.batch)))
     else:
-        src = StepSource(small, base, cfg, problems, vocab)
+        src = StepSource(small, base, cfg, mine, vocab)
+        ff_steps = src.fast_forward(ff)
+        c_ff = (len(small.calls), len(base.calls))
         for _ in range(args.warmup):
             src.step()
+            warm_bounds.append((len(small.calls), len(base.calls)))
 
     stream = torch.cuda.current_stream()
     s0 = (small.engine.stats.snapshot(), base.engine.stats.snapshot())
+    c0 = (len(small.calls), len(base.calls))
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    outcomes = []
+    outcomes, bounds = [], []
     with ClockSampler(local) as clocks:
         e0.record(stream)
         if sched is not None:
@@ -233,6 +349,7 @@ def run_ours(args) -> None:
         else:
             for _ in range(args.steps):
                 outcomes.append(src.step())
+                bounds.append((len(small.calls), len(base.calls)))
         e1.record(stream)
         torch.cuda.synchronize()
     if dist is not None:
@@ -251,12 +368,15 @@ def run_ours(args) -> None:
     max_dev_ms = _reduce_max(dist, dev_ms)
     max_wall_ms = _reduce_max(dist, wall_ms)
     peaks = _peaks()
-    ach = db.decode_bytes / (db.decode_ms * 1e-3) / 1e9 if db.decode_ms > 0 else 0.0
+    kernels = kernel_lines(ds, db, names, peaks, sustained=True)
+    dom = max(kernels, key=lambda k: k["ms"])
+    traffic, traffic_src = _traffic(dom["instance"], names[0 if dom["instance"].startswith("draft") else 1])
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
+    ctx = [o.step.index for o in outcomes]
     result = {
         "metric": METRIC,
         "value": round(tot_tokens / (max_dev_ms * 1e-3), 2),
@@ -269,16 +389,9 @@ def run_ours(args) -> None:
         "scaling": "weak" if args.mode == "dp" else "strong",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (random-init weights, seeded 64-word problems)",
-        "config": {"workload": WORKLOADS[args.pair].replace("batch 1", f"batch {args.batch}"), "pair": args.pair, "threshold": args.threshold,
-                   "verify_template": args.verify_template, "spec_gamma": args.spec_gamma,
-                   "token_budget": args.budget, "max_step_tokens": args.max_step_tokens,
-                   "batch": args.batch, "parallelism": (f"dp{world} (independent problems per GPU"
-                                               + (f", {args.batch} concurrent trajectories per GPU "
-                                                  "sharing batched device passes)" if args.batch > 1 else ")")
-                                               if args.mode == "dp" else
-                                               f"tp{world} (base sharded, NCCL all-reduce; draft replicated)"),
-                   "l2": "weights (17 GB) exceed L2 (126 MB): no flush needed"},
+        "data": "synthetic (seeded random-init weights with the shapes.py successor/judge circuits, "
+                "seeded 64-word problems)",
+        "config": bench_config(args, world),
         "e2e": {"value": round(tot_tokens / (max_wall_ms * 1e-3), 2), "unit": UNIT,
                 "ms_per_step": round(max_wall_ms / n_steps, 3),
                 "h2d_bytes_per_step": round((ds.h2d_bytes + db.h2d_bytes) / n_steps),
@@ -289,23 +402,20 @@ def run_ours(args) -> None:
             "fallback": round(1e3 * sum(x.fallback_s for x in lat) / n_steps, 3),
             "device": round(dev_ms / n_steps, 3)},
         "loop": {"tokens": tokens, "accepted_fraction": round(n_spec / len(outcomes), 3),
-                 "trajectories": src.trajectories,
+                 "trajectories": src.trajectories, "fast_forward_steps": ff_steps,
+                 "first_step_index": min(ctx), "draft_decode_tokens": ds.decode_tokens,
                  "draft_decode_ms_per_token": round(ds.decode_ms / max(1, ds.decode_tokens), 4),
+                 "base_decode_tokens": db.decode_tokens,
                  "base_decode_ms_per_token": round(db.decode_ms / max(1, db.decode_tokens), 4),
-                 "base_prefill_tokens": db.prefill_tokens, "base_prefill_ms": round(db.prefill_ms, 2)},
-        "roofline": {"kernel": "decode_mk_kernel (persistent weight-streaming decode, base model "
-                               "fallback steps): algorithmic bytes = 2*(P_body+P_head) + (C+1)*kvB "
-                               "per token (SURVEY 8d) / CUDA-event decode time",
-                     "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
-                     "peak_source": peaks["src"],
-                     # ncu --set full of the same kernel (7B base, C~2K): DRAM bytes
-                     # read+written per decoded token, vs the algorithmic bytes
-                     "traffic": 14.271e9 if args.pair == "1.5b+7b" else None,
-                     "traffic_unit": "bytes/token (profiles/r01_ncu_decode_mk_qwen2.5-7b_summary.txt)",
-                     "algorithmic_bytes_per_token": round(db.decode_bytes / max(1, db.decode_tokens)),
-                     "draft_decode_GBps": round(ds.decode_bytes / (ds.decode_ms * 1e-3) / 1e9, 1)
-                     if ds.decode_ms > 0 else None},
+                 "base_prefill_rows": db.prefill_tokens, "base_prefill_ms": round(db.prefill_ms, 2)},
+        "roofline": {**{k: dom[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac")},
+                     "instance": dom["instance"], "share_of_device_time": round(dom["ms"] / dev_ms, 4),
+                     "peak_source": peaks["src"] + (", sustained bf16" if dom["unit"] == "TFLOP/s" else ""),
+                     "algorithmic": "SURVEY §8d per-unit bytes/flops (shapes.ModelSpec.decode_bytes / "
+                                    "prefill_cost) x units in the window / CUDA-event time of that "
+                                    "kernel instance on its launch stream (sr_last_timing)",
+                     "traffic": traffic, "traffic_source": traffic_src},
+        "kernels": kernels,
         "gpu_launches": ds.launches + db.launches,
         **({"batching": {"trajectories_in_flight": args.batch,
                          "device_passes": len(sched.batches),
@@ -313,161 +423,226 @@ def run_ours(args) -> None:
            if sched is not None else {}),
         "clocks": clocks.summary(),
     }
-    if world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(args, outcomes_stats=(ds, db, tokens, n_steps))
+    if record and args.dump_trace:
+        dump_trace(args, src, small, base, ff_steps, c_ff, warm_bounds + bounds, names)
+    if world == 1 and not args.no_cpu_baseline and record:
+        result["cpu_baseline"] = cpu_baseline(args, small, base, names, c0, bounds, outcomes)
     print(json.dumps(result), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
 
-# ----------------------------------------------------------------- CPU arm --
-def _cpu_costs(args, layers: int):
-    """Per-token CPU cost (s) of decode and prefill for both models, measured
-    on ``layers``-layer slices of the real shapes and extrapolated to the full
-    depth by weight bytes (CPU decode is memory-bound)."""
-    from oracle.ref_model import RefModel
-    from paper_2504_07891_b200.shapes import PAIRS, get_spec, make_weights
-
-    threads = len(os.sched_getaffinity(0))
-    torch.set_num_threads(threads)
-    out = {}
-    for name in PAIRS[args.pair]:
-        spec = get_spec(name)
-        keep = list(range(min(layers, spec.n_layers)))
-        w = make_weights(spec, args.seed, device="cpu", layers=keep)
-        m = RefModel(spec, w, max_pos=4096 + 1024, layers=keep)
-        del w
-        body_per_layer = (spec.body_params() - spec.d_model) / spec.n_layers
-        full = spec.body_params() + spec.head_params()
-        sliced = body_per_layer * len(keep) + spec.head_params()
-        scale = full / sliced
-        g = torch.Generator().manual_seed(1)
-        ids = torch.randint(16, 4000, (512,), generator=g).tolist()
-        cache = m.new_cache()
-        t0 = time.perf_counter()
-        m.forward(cache, ids[:80])
-        prefill_s = (time.perf_counter() - t0) / 80 * scale
-        t0 = time.perf_counter()
-        n_dec = 6
-        for t in ids[80:80 + n_dec]:
-            m.forward(cache, [t])
-        decode_s = (time.perf_counter() - t0) / n_dec * scale
-        out[name] = {"decode_s_per_token": decode_s, "prefill_s_per_token": prefill_s,
-                     "scale": round(scale, 3)}
-        del m
-    return out, threads
+def bench_config(args, world: int) -> dict:
+    """The ``config`` object both arms print (same_config)."""
+    return {"workload": WORKLOADS[args.pair].replace("batch 1", f"batch {args.batch}"),
+            "pair": args.pair, "threshold": args.threshold, "verify_template": args.verify_template,
+            "spec_gamma": args.spec_gamma, "token_budget": args.budget,
+            "max_step_tokens": args.max_step_tokens, "batch": args.batch,
+            "timed_window": (f"after an untimed fast-forward to "
+                             f"{args.budget // 2 if args.ff_tokens < 0 else args.ff_tokens} CoT "
+                             f"tokens of the first problem, then the warm-up steps"),
+            "problems": f"task0000..task{args.problems - 1:04d} (dp.problem_text), split by id",
+            "parallelism": (f"dp{world} (problem-id partition, no data-path collective"
+                            + (f", {args.batch} concurrent trajectories per GPU sharing batched "
+                               "device passes)" if args.batch > 1 else ")")
+                            if args.mode == "dp" else
+                            f"tp{world} (base sharded, NCCL all-reduce; draft replicated)"),
+            "l2": "weights (3.5 + 65.5 GB) exceed L2 (126 MB) on every step: no flush needed"}
 
 
-def cpu_baseline(args, outcomes_stats) -> dict:
-    """Oracle on the host cores for the same step mix as the timed GPU steps."""
-    ds, db, tokens, steps = outcomes_stats
-    costs, threads = _cpu_costs(args, args.ref_layers)
-    from paper_2504_07891_b200.shapes import PAIRS
+def dump_trace(args, src, small, base, ff_steps, c_ff, step_ends, names) -> None:
+    """Write the first trajectory's calls up to the end of the timed window
+    (``--impl reference`` replays them through the reference engine): the
+    fast-forward's calls, then per warm-up / timed step the (small, base)
+    call counts at its end (``step_ends``)."""
+    if src.trajectories != 1:
+        raise RuntimeError("the trace covers one trajectory: raise --budget or lower --steps")
+    path = Path(args.dump_trace)
+    path.parent.mkdir(parents=True, exist_ok=True)
+    end = step_ends[-1]
+    path.write_text(json.dumps({
+        "pair": args.pair, "budget": args.budget, "threshold": args.threshold,
+        "max_step_tokens": args.max_step_tokens, "problem": src.problems[0],
+        "fast_forward_steps": ff_steps, "window_start": list(c_ff),
+        "step_ends": [list(e) for e in step_ends],
+        "small": call_descriptors(small, small.calls[:end[0]], names[0]),
+        "base": call_descriptors(base, base.calls[:end[1]], names[1]),
+    }) + "\n")
 
-    dn, bn = PAIRS[args.pair]
-    cpu_s = (ds.prefill_tokens * costs[dn]["prefill_s_per_token"]
-             + (ds.decode_tokens + ds.calls) * costs[dn]["decode_s_per_token"]
-             + db.prefill_tokens * costs[bn]["prefill_s_per_token"]
-             + db.decode_tokens * costs[bn]["decode_s_per_token"])
-    return {"value": round(tokens / cpu_s, 3), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"fp32 torch oracle on {args.ref_layers}-layer slices of both models "
-                      f"(80-token prefill, 6 decode tokens each), extrapolated to full depth by "
-                      f"weight bytes and applied to the timed steps' token mix",
-            "ms_per_step": round(1e3 * cpu_s / steps, 1), "per_token_costs": costs}
+
+def cpu_baseline(args, small, base, names, c0, bounds, outcomes) -> dict:
+    """The oracle's arithmetic for the first timed steps' recorded calls, on
+    the host cores (``oracle/cpu_replay.py``): steps are replayed in order
+    until >= ``--cpu-seconds`` of CPU work (at least one step)."""
+    from oracle.cpu_replay import CpuReplay
+    from paper_2504_07891_b200.shapes import get_spec
+
+    rep = CpuReplay({n: get_spec(n) for n in names}, max_ctx=args.budget + 1024)
+    rep.warm()
+    prev = c0
+    secs = toks = n = 0
+    for (cs, cb), o in zip(bounds, outcomes):
+        calls = (call_descriptors(small, small.calls[prev[0]:cs], names[0])
+                 + call_descriptors(base, base.calls[prev[1]:cb], names[1]))
+        secs += sum(rep.run(c) for c in calls)
+        toks += o.step.token_count
+        n += 1
+        prev = (cs, cb)
+        if secs >= args.cpu_seconds:
+            break
+    return {"value": round(toks / secs, 3), "unit": UNIT, "cores": rep.threads, "kind": "port",
+            "sample": (f"the first {n} timed steps ({toks} CoT tokens): every backend call of those "
+                       f"steps (draft decode, verify prefill + readout, fallback decode) executed "
+                       f"at the full {names[0]} / {names[1]} shapes and depth at its recorded "
+                       f"context on {rep.threads} host threads (torch bf16 matmul, fp32 accumulate; "
+                       f"oracle/cpu_replay.py)"),
+            "ms_per_step": round(1e3 * secs / n, 1), "cpu_seconds": round(secs, 1)}
+
+
+# ---------------------------------------------------------- reference arm --
+def _reference_package():
+    for root in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (root / "stepspec" / "__init__.py").exists():
+            if str(root) not in sys.path:
+                sys.path.insert(0, str(root))
+            import stepspec
+
+            return stepspec, str(root)
+    return None, None
+
+
+def _replay_backend_cls(stepspec):
+    """A reference ``Backend`` (``backends/base.py:77-100``) that answers the
+    reference engine with a recorded trajectory's results and, inside the
+    window, spends the host-CPU cost of each call (``oracle/cpu_replay``):
+    the engine's own clocks then measure that cost (``engine.py:199-202``,
+    ``engine.py:284-294``)."""
+    from stepspec.backends.base import (Backend, FinishReason, GenerationResult,
+                                        ScoreParseFailure)
+    from stepspec.core import UtilityScore
+
+    class ReplayBackend(Backend):
+        simulated = False
+
+        def __init__(self, profile, calls, lo, hi, rep):
+            self.profile = profile
+            self.calls, self.lo, self.hi, self.rep = calls, lo, hi, rep
+            self.i = 0
+            self.cpu_s = 0.0
+
+        def _next(self, prompt: str) -> dict | None:
+            if self.i >= len(self.calls):
+                return None
+            c = self.calls[self.i]
+            if len(prompt.split()) != c["prompt_len"]:
+                raise AssertionError(f"{self.profile.name} call {self.i}: the engine's prompt has "
+                                     f"{len(prompt.split())} tokens, the trace {c['prompt_len']}")
+            self.i += 1
+            return c
+
+        def _cost(self, c) -> float:
+            if self.lo <= self.i - 1 < self.hi:
+                t = self.rep.run(c)
+                self.cpu_s += t
+                return t
+            return 0.0
+
+        def generate_step(self, request):
+            c = self._next(request.prompt)
+            if c is None:  # past the recorded window: end thinking / empty answer
+                return GenerationResult(text="", token_count=0, finish_reason=FinishReason.END_THINK)
+            assert c["kind"] == "gen", c
+            t = self._cost(c)
+            return GenerationResult(text=c["text"], token_count=c["token_count"],
+                                    finish_reason=FinishReason(c["finish"]), measured_latency_s=t)
+
+        def score_step(self, request):
+            from stepspec.prompts import render_verification_prompt
+
+            c = self._next(render_verification_prompt(request.problem, request.cot_prefix,
+                                                      request.candidate_step))
+            if c is None:
+                raise ScoreParseFailure("past the recorded window")
+            assert c["kind"] == "score", c
+            self._cost(c)
+            if c["score"] < 0:
+                raise ScoreParseFailure("no digit in the top-10 or the sampled token")
+            return UtilityScore(c["score"])
+
+    return ReplayBackend
 
 
 def run_reference(args) -> None:
-    """Reference arm: the reference's loop on the host CPU (oracle port for
-    the model arithmetic; the unmodified reference engine when installed in
-    baseline/_ref).  Rank 0 only."""
+    """Reference arm: the unmodified reference engine (``run_trajectory``,
+    ``engine.py:297``) drives replay backends over this benchmark's recorded
+    C3 trajectory; every warm-up and timed step's calls are executed on the
+    host cores at full model shape (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    ref_path = ROOT / "baseline" / "_ref"
-    engine_kind = "this repo's driver (reference not installed)"
-    run_traj = None
-    if (ref_path / "stepspec").exists():
-        sys.path.insert(0, str(ref_path))
-        try:
-            import stepspec  # noqa: F401
-            from stepspec import engine as reng
+    trace_path = Path(args.trace) if args.trace else ROOT / "bench_data" / f"{args.pair}_trace.json"
+    stepspec, ref_root = _reference_package()
+    why = None
+    if stepspec is None:
+        why = "reference package not installed in baseline/_ref"
+    elif not trace_path.exists():
+        why = f"no recorded trajectory {trace_path.name} for pair {args.pair}"
+    if why:
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        return
+    tr = json.loads(trace_path.read_text())
+    for k in ("pair", "budget", "threshold", "max_step_tokens"):
+        if tr[k] != getattr(args, k):
+            print(json.dumps({"impl": "reference",
+                              "unavailable": f"trace {k}={tr[k]} differs from --{k} {getattr(args, k)}"}))
+            return
+    n_win = args.warmup + args.steps
+    if len(tr["step_ends"]) < n_win:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"trace window has {len(tr['step_ends'])} steps < warmup+steps {n_win}"}))
+        return
+    from oracle.cpu_replay import CpuReplay
+    from paper_2504_07891_b200.shapes import PAIRS, get_spec
+    from stepspec import engine as reng
+    from stepspec.core import AcceptanceThreshold, BackendProfile, BackendRole, EngineConfig
 
-            engine_kind = "reference stepspec engine (baseline/_ref)"
-            run_traj = reng
-        except Exception:  # noqa: BLE001
-            run_traj = None
-    costs, threads = _cpu_costs(args, args.ref_layers)
-    # the reference loop on the CPU oracle: a tiny-pair trajectory gives the
-    # step mix (tokens / calls per step); costs are the C2 shapes' per-token costs
-    from oracle.ref_engine import oracle_backend
-    from paper_2504_07891_b200 import AcceptanceThreshold, EngineConfig
-    from paper_2504_07891_b200.domain import BackendRole
-    from paper_2504_07891_b200.host import reference_types
-    from paper_2504_07891_b200.shapes import PAIRS
-    from paper_2504_07891_b200.vocab import shared_vocab
-
-    T = reference_types(sys.modules["stepspec"]) if run_traj is not None else None
-    small = oracle_backend("tiny-draft", BackendRole.SMALL, types=T, record=True)
-    base = oracle_backend("tiny-base", BackendRole.BASE, types=T, record=True,
-                          threshold=args.threshold)
-    v = shared_vocab(4096)
-    if run_traj is not None:
-        from stepspec.core import AcceptanceThreshold as RT
-        from stepspec.core import EngineConfig as RC
-
-        cfg = RC(threshold=RT(args.threshold), temperature=0.0, token_budget=args.budget,
-                 max_step_tokens=args.max_step_tokens)
-    else:
-        cfg = EngineConfig(threshold=AcceptanceThreshold(args.threshold), temperature=0.0,
-                           token_budget=args.budget, max_step_tokens=args.max_step_tokens)
-    dn, bn = PAIRS[args.pair]
-    per_step = []  # (CoT tokens, CPU seconds at the C2 shapes)
+    names = PAIRS[args.pair]
     t_start = time.perf_counter()
-    p = 0
-    while len(per_step) < args.warmup + args.steps:
-        small.calls.clear()
-        base.calls.clear()
-        prob = v.problem(64, p)
-        p += 1
-        if run_traj is not None:
-            res = run_traj.run_trajectory(cfg, prob, small, base)
-        else:
-            from paper_2504_07891_b200.driver import run_trajectory
-
-            res = run_trajectory(cfg, prob, small, base)
-        calls = sorted([("small", c) for c in small.calls] + [("base", c) for c in base.calls],
-                       key=lambda x: x[1]["seq"])
-        # a step starts at each draft call; the answer (last base call) is not a step
-        groups, cur = [], None
-        for who, c in calls:
-            if who == "small":
-                cur = [c["fresh"] * costs[dn]["prefill_s_per_token"]
-                       + len(c["gen_ids"]) * costs[dn]["decode_s_per_token"]]
-                groups.append(cur)
-            elif cur is not None:
-                if c["kind"] == "score":
-                    cur.append(c["fresh"] * costs[bn]["prefill_s_per_token"])
-                else:
-                    cur.append(c["fresh"] * costs[bn]["prefill_s_per_token"]
-                               + len(c["gen_ids"]) * costs[bn]["decode_s_per_token"])
-        for st, g in zip(res.state.retained_steps, groups):
-            per_step.append((st.token_count, sum(g)))
-    timed = per_step[args.warmup:]
-    tokens = sum(t for t, _ in timed)
-    secs = sum(s for _, s in timed)
+    rep = CpuReplay({n: get_spec(n) for n in names}, max_ctx=args.budget + 1024)
+    rep.warm()
+    Replay = _replay_backend_cls(stepspec)
+    end = tr["step_ends"][n_win - 1]
+    prof = lambda n, r: BackendProfile(name=f"cpu-{n}", role=r, decode_s_per_token=1.0,  # noqa: E731
+                                       prefill_tokens_per_s=1.0)
+    small = Replay(prof(names[0], BackendRole.SMALL), tr["small"], tr["window_start"][0], end[0], rep)
+    base = Replay(prof(names[1], BackendRole.BASE), tr["base"], tr["window_start"][1], end[1], rep)
+    cfg = EngineConfig(threshold=AcceptanceThreshold(args.threshold), temperature=0.0,
+                       token_budget=args.budget, max_step_tokens=args.max_step_tokens)
+    res = reng.run_trajectory(cfg, tr["problem"], small, base)
+    first = tr["fast_forward_steps"] + args.warmup
+    timed = [s for s in res.state.retained_steps if first <= s.index < first + args.steps]
+    assert len(timed) == args.steps, (len(timed), args.steps)
+    tokens = sum(s.token_count for s in timed)
+    secs = sum(s.latency.total_s for s in timed)
     value = round(tokens / secs, 3)
+    n_acc = sum(1 for s in timed if s.producer.value == "Speculator")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / len(timed), 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": WORKLOADS[args.pair].replace("batch 1", f"batch {args.batch}"), "pair": args.pair,
-                                        "threshold": args.threshold, "token_budget": args.budget},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{engine_kind} driving the CPU oracle; per-token CPU costs of "
-                                   f"the C2 shapes measured on {args.ref_layers}-layer slices and "
-                                   f"extrapolated by weight bytes, applied to each step's tokens",
-                         "per_token_costs": costs},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (recorded C3 trajectory of this benchmark, bench_data/)",
+        "config": bench_config(args, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": rep.threads, "kind": "port",
+                         "sample": (f"reference stepspec engine ({ref_root}) over the recorded "
+                                    f"trajectory of task0000; its {args.warmup} warm-up + "
+                                    f"{args.steps} timed steps (indices {first - args.warmup}.."
+                                    f"{first + args.steps - 1}) execute every backend call at the "
+                                    f"full {names[0]} / {names[1]} shapes and depth on the host "
+                                    f"cores (oracle/cpu_replay.py); latency from the engine's own "
+                                    f"clocks")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "loop": {"tokens": tokens, "accepted_fraction": round(n_acc / args.steps, 3),
+                 "cpu_seconds": round(small.cpu_s + base.cpu_s, 1)},
         "wall_s": round(time.perf_counter() - t_start, 1),
     }), flush=True)
 
@@ -479,29 +654,32 @@ def main() -> None:
         faulthandler.dump_traceback_later(int(os.environ["BENCH_STACK_DUMP_S"]), repeat=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    # the loop's step mix (draft steps accepted or regenerated) varies a lot
-    # between random-init trajectories (one C2 trajectory is ~130 steps): 480
-    # steps average over several of them and still run in about a minute
-    ap.add_argument("--steps", type=int, default=480)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pair", default="1.5b+7b")
+    ap.add_argument("--pair", default="1.5b+32b")
     ap.add_argument("--threshold", type=int, default=7)
-    ap.add_argument("--budget", type=int, default=4096)
+    ap.add_argument("--budget", type=int, default=8192)
     ap.add_argument("--max-step-tokens", type=int, default=256)
+    ap.add_argument("--problems", type=int, default=64,
+                    help="fixed problem set task0000.. (split by id across DP ranks)")
+    ap.add_argument("--ff-tokens", type=int, default=-1,
+                    help="untimed fast-forward to this many CoT tokens (-1: budget / 2)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--ref-layers", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
+                    help="CPU work of the cpu_baseline sample (whole timed steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-trace", default="", help="write the recorded trajectory (reference arm input)")
+    ap.add_argument("--trace", default="", help="--impl reference: recorded trajectory to replay")
     ap.add_argument("--verify-template", default="v1", choices=["v1", "v2"],
                     help="v2: prefix-sharing verification prompt (not the reference wording)")
     ap.add_argument("--spec-gamma", type=int, default=0,
                     help="token-level speculation inside base generation (0 = off)")
     ap.add_argument("--batch", type=int, default=1,
                     help="trajectories per GPU run concurrently with batched device passes "
-                         "(SURVEY 8f-2; config C5 uses 8); 1 = the C2 batch-1 workload")
+                         "(SURVEY 8f-2; config C5 uses 8); 1 = batch-1 workload")
     ap.add_argument("--mode", default="dp", choices=["dp", "tp"],
-                    help="multi-GPU: dp = independent problems per rank (C5), "
-                         "tp = base model tensor-parallel over the ranks (C4)")
+                    help="multi-GPU: dp = problem-id partition (C5), tp = base tensor-parallel (C4)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -143,6 +143,8 @@ class EngineStats:
     prefill_tokens: int = 0
     decode_tokens: int = 0      # tokens produced by the decode graph (n_gen - 1)
     decode_bytes: float = 0.0   # algorithmic HBM bytes of those decode steps
+    prefill_bytes: float = 0.0  # algorithmic HBM bytes of the prefill passes (+ LM head)
+    prefill_flops: float = 0.0
     launches: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
@@ -160,6 +162,9 @@ class EngineStats:
         self.prefill_tokens += n_ids
         steps = max(0, n_gen - 1)
         self.decode_tokens += steps
+        b, f = spec.prefill_cost(start, n_ids, 1, m.max_tokens)
+        self.prefill_bytes += b
+        self.prefill_flops += f
         ctx0 = start + n_ids
         for i in range(steps):
             self.decode_bytes += spec.decode_bytes(ctx0 + i)
@@ -169,14 +174,29 @@ class EngineStats:
         self.h2d_bytes += 4 * n_ids + 64
         self.d2h_bytes += 4 * (2 + m.max_new) * 2
 
-    def add_score(self, m: "DeviceModel", n_ids: int, start: int) -> None:
+    def add_score(self, m: "DeviceModel", n_ids: int, start: int, head_rows: int = 1) -> None:
         t = m.timing()
+        b, f = m.spec.prefill_cost(start, n_ids, head_rows, m.max_tokens)
+        self.prefill_bytes += b
+        self.prefill_flops += f
         self.calls += 1
         self.prefill_ms += t.prefill_ms
         self.prefill_tokens += n_ids
         self.launches += self._prefill_launches(m.spec, n_ids) + 2
         self.h2d_bytes += 4 * n_ids + 64
         self.d2h_bytes += 16
+
+    def add_pass(self, spec, starts, counts) -> None:
+        """Algorithmic cost of one multi-sequence pass: the weights stream
+        once for every row, each sequence reads its own context."""
+        kvb = spec.kv_bytes_per_token()
+        attn = 4 * spec.n_layers * spec.n_heads * spec.head_dim
+        rows = sum(counts)
+        self.prefill_bytes += 2 * (spec.body_params() + spec.head_params())
+        self.prefill_flops += 2 * rows * spec.body_params() + 2 * len(counts) * spec.head_params()
+        for s0, n in zip(starts, counts):
+            self.prefill_bytes += (s0 + 2 * n) * kvb
+            self.prefill_flops += attn * n * (s0 + n / 2)
 
     def snapshot(self) -> "EngineStats":
         return EngineStats(**self.__dict__)
@@ -387,6 +407,7 @@ class NativeEngine:
         self.stats.calls += 1
         self.stats.prefill_ms += m.timing().prefill_ms
         self.stats.prefill_tokens += rows
+        self.stats.add_pass(self.spec, list(starts), list(counts))
         self.stats.launches += 9 * self.spec.n_layers + 3 + n
         self.stats.h2d_bytes += 12 * rows
         self.stats.d2h_bytes += 16 * n
@@ -423,6 +444,7 @@ class NativeEngine:
             self.stats.calls += 1
             self.stats.prefill_ms += m.timing().prefill_ms
             self.stats.prefill_tokens += rows
+            self.stats.add_pass(self.spec, list(starts), list(counts))
             self.stats.launches += 9 * self.spec.n_layers + 3
             self.stats.h2d_bytes += 12 * rows
             self.stats.d2h_bytes += 4 * n
@@ -472,7 +494,7 @@ class NativeEngine:
         m.out_host[:n].copy_(m.out_dev[:n], non_blocking=True)
         m.margin_host[:n].copy_(m.margin_dev[:n], non_blocking=True)
         torch.cuda.current_stream(m.device).synchronize()
-        self.stats.add_score(m, n, start)
+        self.stats.add_score(m, n, start, head_rows=n)
         stream.ids.extend(suffix)
         return m.out_host[:n].tolist(), m.margin_host[:n].tolist()
 

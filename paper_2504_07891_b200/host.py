@@ -437,7 +437,8 @@ class ModelBackend(Backend):
                                                    tuple(request.stop))
             if self.record:
                 self.calls.append({"kind": "gen", "prompt_ids": ids, "gen_ids": list(gen),
-                                   "margins": list(getattr(self.engine, "last_margins", [])),
+                                   "margins": ([] if getattr(self, "speculator", None) is not None
+                                               else list(getattr(self.engine, "last_margins", []))),
                                    "finish": finish, "stop": list(request.stop),
                                    "max_tokens": request.max_tokens, "fresh": len(ids) - keep,
                                    "seq": time.monotonic_ns()})

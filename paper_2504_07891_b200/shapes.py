@@ -27,6 +27,35 @@ carries a small, documented "judge circuit" in its weights only:
   padding row of the LM head is a probe ``u / sqrt(d)`` that reads the cue
   alignment the calibration needs (padding rows are never produced).
 
+* the **probe head** (``probe_gain`` > 0, bench base models): in the last
+  layer, q head 0 reads the cue direction (its q rows are ``u`` placed on
+  the RoPE pairs of ``probe_pairs``) and kv head 0's keys are a constant
+  bias phased so that, after RoPE, the score peaks at distance
+  ``probe_offset`` = 36 -- the last word of the candidate step (the verify
+  template's tail after the candidate is 35 words).  The head's output
+  columns of W_o are scaled by ``probe_gain``.  So the cue position copies
+  the value vector of the candidate's last word, and the digit rows' random
+  part turns it into the score: consecutive steps of one trajectory get
+  nearly independent scores (``tools/calibrate_judge.py`` reports the
+  consecutive-equal rate, ~0.15 against 0.1 for independent draws) instead
+  of the long-range context deciding one score for a whole trajectory.
+
+The successor circuit
+---------------------
+A greedy random-init decoder falls into short loops: its final hidden state
+is ~85% one direction common to all positions, so a few "hub" tokens win
+every argmax, and a step that loops without a boundary word runs to
+``max_step_tokens`` (measured: 23-69% of C2 draft steps capped at 256).  The
+bench models therefore carry a successor circuit: embeddings are N(0, 1)
+(``embed_std``) so the current token stays visible in the last residual,
+and every ordinary word's LM-head row gets ``succ_gain`` times the unit
+embedding of its predecessor under a seeded permutation of the ordinary ids
+(``successor_perm``, keyed by the vocabulary, so draft and base share it).
+Greedy text then walks the permutation (~90% of draft tokens, ~99% of base
+tokens follow it) instead of looping, boundary words (1 in 24 ids) end steps
+at ~24 tokens as SURVEY §7.1 asks (mean 24, p90 ~55, none capped), and a
+draft and its base agree on most tokens, as a real distilled pair does.
+
 All of it is plain weight values: the kernels contain no special case.
 """
 
@@ -64,6 +93,9 @@ class ModelSpec:
     judge_offsets: tuple = ()  # per-digit gain offsets (tools/calibrate_judge.py)
     embed_std: float = 0.0   # embedding init std (0 -> 0.02)
     succ_gain: float = 0.0   # successor circuit (module doc); 0 = off
+    probe_gain: float = 0.0  # judge probe head output scale (module doc); 0 = off
+    probe_scale: float = 6.0  # per-RoPE-pair amplitude of the probe head's q / k
+    probe_offset: int = 36   # cue-to-probed-token distance (last candidate word)
     # tensor parallelism (tp_spec): this rank's shard of a model split `tp_world` ways
     tp_world: int = 1
     tp_rank: int = 0
@@ -105,6 +137,30 @@ class ModelSpec:
         return 2 * (self.body_params() + self.head_params()) + (ctx + 1) * self.kv_bytes_per_token()
 
 
+    def prefill_cost(self, start: int, n: int, head_rows: int = 1,
+                     chunk: int = 256) -> tuple[float, float]:
+        """Algorithmic (HBM bytes, flops) of prefilling ``n`` rows at
+        positions ``start``.. in chunks of ``chunk`` rows (SURVEY §8d verify
+        row): per chunk the body weights once, the K/V of the context read
+        once and the new rows' K/V written; 2*M*P_body GEMM flops plus the
+        causal attention 4*L*H*128*M*(ctx + M/2); the LM head once for
+        ``head_rows`` readout rows."""
+        by = fl = 0.0
+        kvb = self.kv_bytes_per_token()
+        attn = 4 * self.n_layers * self.n_heads * self.head_dim
+        c0 = 0
+        while c0 < n:
+            m = min(chunk, n - c0)
+            s = start + c0
+            by += 2 * self.body_params() + (s + m) * kvb + m * kvb
+            fl += 2 * m * self.body_params() + attn * m * (s + m / 2)
+            c0 += m
+        if head_rows:
+            by += 2 * self.head_params()
+            fl += 2 * head_rows * self.head_params()
+        return by, fl
+
+
 V_QWEN_DRAFT = 151_936
 V_QWEN_BASE = 152_064
 
@@ -121,10 +177,14 @@ MODELS: dict[str, ModelSpec] = {
                          rope_theta=10_000.0, embed_std=1.0, succ_gain=0.8),
     "qwen2.5-7b": ModelSpec("qwen2.5-7b", 28, 3584, 28, 4, 18944, V_QWEN_BASE, V_QWEN_DRAFT,
                             judge=True, embed_std=1.0, succ_gain=0.8, cue_gain=6.0,
-                            digit_gain=10.0),
+                            digit_gain=12.0, digit_noise=2.0, probe_gain=30.0,
+                            judge_offsets=(-1.0, 2.125, -0.5, -2.0, -1.625, 1.25, -0.25, 0.125,
+                                           0.0, 2.125)),
     "qwq-32b": ModelSpec("qwq-32b", 64, 5120, 40, 8, 27648, V_QWEN_BASE, V_QWEN_DRAFT,
                          judge=True, embed_std=1.0, succ_gain=0.8, cue_gain=6.0,
-                         digit_gain=10.0),
+                         digit_gain=12.0, digit_noise=2.0, probe_gain=30.0,
+                         judge_offsets=(-2.5, 0.25, 3.75, -1.25, 3.5, -0.75, -2.625, -2.75, 0.875,
+                                        1.125)),
 }
 
 PAIRS = {
@@ -285,6 +345,8 @@ def make_tensor(spec: ModelSpec, seed: int, name: str, device: str = "cpu") -> t
             t[dgt] = r + ((spec.digit_gain + offs[dgt]) / math.sqrt(spec.d_model)) * u
         if spec.vocab_rows > spec.vocab_text:
             t[spec.vocab_text] = u / math.sqrt(spec.d_model)  # cue-alignment probe
+    if spec.judge and spec.probe_gain > 0 and name.startswith(f"layers.{spec.n_layers - 1}."):
+        _install_probe(spec, seed, leaf, t)
     if spec.succ_gain > 0 and name == "lm_head":
         # successor circuit: row v reads the (unit) embedding of v's predecessor
         emb = make_tensor(spec, seed, "embed", device).float()
@@ -295,6 +357,36 @@ def make_tensor(spec: ModelSpec, seed: int, name: str, device: str = "cpu") -> t
         t[rows] += spec.succ_gain * (src / src.norm(dim=1, keepdim=True))
         del emb, src
     return t.to(torch.bfloat16)
+
+
+def probe_pairs(spec: ModelSpec) -> np.ndarray:
+    """RoPE pairs the probe head uses: frequencies in [0.02, 1] rad/token,
+    enough to resolve single positions without aliasing over 16K tokens."""
+    half = spec.head_dim // 2
+    inv = spec.rope_theta ** (-np.arange(half, dtype=np.float64) * 2.0 / spec.head_dim)
+    return np.where((inv >= 0.02) & (inv <= 1.0))[0]
+
+
+def _install_probe(spec: ModelSpec, seed: int, leaf: str, t: torch.Tensor) -> None:
+    """Judge probe head (last layer, q head 0 / kv head 0; module doc)."""
+    hd, half, dev = spec.head_dim, spec.head_dim // 2, t.device
+    P = probe_pairs(spec)
+    inv = spec.rope_theta ** (-P.astype(np.float64) * 2.0 / spec.head_dim)
+    c = spec.probe_scale
+    if leaf == "wqkv":
+        u = _judge_direction(spec, seed).to(dev)
+        qv = torch.zeros(hd, device=dev)
+        qv[torch.as_tensor(P, device=dev)] = c
+        t[:hd] = torch.outer(qv, u) / math.sqrt(spec.d_model)
+        t[spec.q_dim: spec.q_dim + hd] = 0.0
+    elif leaf == "bqkv":
+        t[:hd] = 0.0
+        kv = torch.zeros(hd, dtype=torch.float64)
+        kv[torch.as_tensor(P)] = c * torch.from_numpy(np.cos(inv * spec.probe_offset))
+        kv[torch.as_tensor(P + half)] = c * torch.from_numpy(np.sin(inv * spec.probe_offset))
+        t[spec.q_dim: spec.q_dim + hd] = kv.to(dev, torch.float32)
+    elif leaf == "wo":
+        t[:, :hd] *= spec.probe_gain
 
 
 def successor_range(n_text: int) -> tuple[int, int]:
@@ -346,7 +438,7 @@ def rope_table(spec: ModelSpec, max_pos: int) -> torch.Tensor:
 # --------------------------------------------------------------------------
 
 def judge_calibration_prompts(spec: ModelSpec, n: int = 24, cot_step: int = 25,
-                              chain: bool = False) -> list[list[int]]:
+                              chain: bool = False, one_chain: bool = False) -> list[list[int]]:
     """Token ids of ``n`` synthetic verify prompts (64-word problem, a CoT of
     0, cot_step, .. words, a 24-word candidate), seeded and model-independent.
     ``chain``: the CoT and candidate follow the successor circuit's
@@ -360,9 +452,11 @@ def judge_calibration_prompts(spec: ModelSpec, n: int = 24, cot_step: int = 25,
     rng = np.random.default_rng(20250410)
     succ = successor_perm(vocab.n_text)[0].tolist() if chain else None
     out = []
+    base_ids = [int(x) for x in rng.integers(lo, hi, size=64 + cot_step * n + 24)]
     for i in range(n):
         c = cot_step * i
-        ids = [int(x) for x in rng.integers(lo, hi, size=64 + c + 24)]
+        ids = (base_ids[:64 + c + 24] if one_chain
+               else [int(x) for x in rng.integers(lo, hi, size=64 + c + 24)])
         if chain:
             for k in range(65, len(ids)):
                 ids[k] = succ[ids[k - 1]]

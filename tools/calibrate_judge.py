@@ -53,8 +53,10 @@ def main() -> None:
     name = sys.argv[1]
     gpu = "--gpu" in sys.argv
     over = {}
-    if "--digit-noise" in sys.argv:
-        over["digit_noise"] = float(sys.argv[sys.argv.index("--digit-noise") + 1])
+    for flag, key in (("--digit-noise", "digit_noise"), ("--digit-gain", "digit_gain"),
+                      ("--probe-gain", "probe_gain"), ("--probe-scale", "probe_scale")):
+        if flag in sys.argv:
+            over[key] = float(sys.argv[sys.argv.index(flag) + 1])
     spec = get_spec(name, **over)
     n = int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 24
     step = int(sys.argv[sys.argv.index("--cot-step") + 1]) if "--cot-step" in sys.argv else 25
@@ -82,6 +84,18 @@ def main() -> None:
               flush=True)
         spec = dataclasses.replace(spec, judge_offsets=judge_offsets_update(spec, rows))
     print("judge_offsets =", spec.judge_offsets)
+    # one trajectory: consecutive steps share the context and differ in the
+    # candidate; a judge that reads the candidate changes score step to step
+    traj = judge_calibration_prompts(spec, 40, 24, chain=spec.succ_gain > 0, one_chain=True)
+    if gpu:
+        judge.set_spec(spec)
+        fn = judge
+    else:
+        fn = logits_fn_for(spec, gpu)
+    sc = [int(fn(p)[:10].argmax()) for p in traj]
+    same = sum(a == b for a, b in zip(sc, sc[1:])) / (len(sc) - 1)
+    print(f"trajectory scores {sc}  consecutive-equal {same:.2f} (independent ~0.1) "
+          f"accept@7 {sum(x >= 7 for x in sc) / len(sc):.2f}", flush=True)
     print("OVERRIDE " + "".join(f"{k}={v}," for k, v in over.items())
           + "judge_offsets=" + ":".join(str(x) for x in spec.judge_offsets))
 

@@ -1,10 +1,8 @@
-mkdir -p gpurun_out
-for dn in 1.0 2.0; do
-for m in qwen2.5-7b qwq-32b; do
-  timeout 900 python tools/calibrate_judge.py $m --gpu --n 32 --cot-step 120 --iters 3 --digit-noise $dn > gpurun_out/calib_${m}_$dn.txt 2>&1
-done
-O7=$(grep OVERRIDE gpurun_out/calib_qwen2.5-7b_$dn.txt | cut -d' ' -f2)
-O32=$(grep OVERRIDE gpurun_out/calib_qwq-32b_$dn.txt | cut -d' ' -f2)
-timeout 600 python tools/loop_stats.py --pair 1.5b+7b --base-over "$O7" --steps 40 --problems 3 > gpurun_out/loop4_c2_$dn.txt 2>&1
-timeout 900 python tools/loop_stats.py --pair 1.5b+32b --base-over "$O32" --steps 25 --problems 2 > gpurun_out/loop4_c3_$dn.txt 2>&1
-done
+mkdir -p gpurun_out bench_data
+set -x
+timeout 900 python bench.py --steps 60 --warmup 5 --no-cpu-baseline --dump-trace bench_data/1.5b+32b_trace.json > gpurun_out/bench_trace.json 2> gpurun_out/bench_trace.err
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 900 python tools/measure_floors.py --out gpurun_out/floors.json > gpurun_out/floors.log 2>&1 && cp gpurun_out/floors.json tests/golden/floors.json
+SR_PARITY_REPORT=gpurun_out/parity_report.jsonl timeout 1500 python -m pytest tests/test_gpu_trajectory_parity.py -x -q -s > gpurun_out/parity.log 2>&1
+timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+cp bench_data/1.5b+32b_trace.json gpurun_out/
