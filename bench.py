@@ -432,6 +432,39 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+def run_sweep(args) -> None:
+    """Config C5 as the reference's ``run_sweep`` (``bench.py:221-300``): the
+    fixed problem set split by problem id over the ranks (``dp.partition``),
+    every (threshold, problem) SpecReason trajectory plus BaseOnly, records
+    gathered on rank 0; asserts threshold 10 == BaseOnly per problem
+    (``test_acceptance.py:104-113``) and prints the per-cell summary."""
+    from paper_2504_07891_b200 import AcceptanceThreshold, EngineConfig, Scheme
+    from paper_2504_07891_b200.backend import build_pair
+    from paper_2504_07891_b200.dp import (cells, check_forced_reject, gather, partition,
+                                          problem_ids, run_partition)
+
+    dist, rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    small, base = build_pair(args.pair, seed=args.seed, max_ctx=args.budget + 512,
+                             threshold=args.threshold)
+    cfg = EngineConfig(threshold=AcceptanceThreshold(args.threshold), temperature=0.0,
+                       token_budget=args.budget, max_step_tokens=args.max_step_tokens)
+    values = [int(x) for x in args.sweep.split(",")]
+    mine = partition(problem_ids(args.problems), rank, world)
+    t0 = time.perf_counter()
+    recs = run_partition(mine, small, base, cfg, values, schemes=(Scheme.SPEC_REASON, Scheme.BASE_ONLY))
+    secs = _reduce_max(dist, time.perf_counter() - t0)
+    allrecs = gather(recs, dist)
+    if rank == 0:
+        n_checked = check_forced_reject(allrecs) if 10 in values else 0
+        print(json.dumps({"sweep": values, "pair": args.pair, "budget": args.budget,
+                          "problems": args.problems, "n_gpus": world,
+                          "forced_reject_equals_base_only": n_checked,
+                          "cells": cells(allrecs), "wall_s": round(secs, 1)}), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def bench_config(args, world: int) -> dict:
     """The ``config`` object both arms print (same_config)."""
     return {"workload": WORKLOADS[args.pair].replace("batch 1", f"batch {args.batch}"),
@@ -678,6 +711,9 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=1,
                     help="trajectories per GPU run concurrently with batched device passes "
                          "(SURVEY 8f-2; config C5 uses 8); 1 = batch-1 workload")
+    ap.add_argument("--sweep", default="",
+                    help="C5 threshold sweep, e.g. 3,5,7,9,10: every problem of --problems at every "
+                         "threshold plus BaseOnly (problem-id partition over the ranks)")
     ap.add_argument("--mode", default="dp", choices=["dp", "tp"],
                     help="multi-GPU: dp = problem-id partition (C5), tp = base tensor-parallel (C4)")
     args = ap.parse_args()
@@ -685,6 +721,8 @@ def main() -> None:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
         run_reference(args)
+    elif args.sweep:
+        run_sweep(args)
     else:
         run_ours(args)
 

@@ -214,6 +214,30 @@ int sr_tp_comm_create(const uint8_t* h_id128, int32_t world, int32_t rank, void*
 int sr_tp_comm_destroy(void* comm);
 int sr_model_set_tp(void* model, void* comm);
 
+/*
+ * Tensor parallelism over NVLink peer memory (no NCCL).  Each rank creates
+ * one exchange buffer (sr_tp_peer_create: max_elems floats per rank for the
+ * host-driven collectives -- at least max_tokens * d_model -- and dec_row >=
+ * d_model floats per rank for the decode kernel's mailbox), shares it with
+ * the other ranks (sr_tp_peer_handle / sr_tp_peer_open over CUDA IPC across
+ * processes; sr_tp_peer_base / sr_tp_peer_attach within one process) and
+ * attaches it to its model (sr_model_set_tp_peer).  With it the persistent
+ * decode kernel decodes a tensor-parallel step itself: after the O and down
+ * phases each CTA stores its rows of the rank's partial residual update into
+ * every rank's mailbox and the ranks sum them in rank order; the greedy
+ * choice merges every rank's (top-1, index, top-2).  Prefill and the judge
+ * readout use one-shot peer all-reduce / all-gather / broadcast kernels, or
+ * NCCL when a communicator is attached too.
+ */
+int sr_tp_peer_create(int32_t world, int32_t rank, int64_t max_elems, int32_t dec_row,
+                      void** out_peer);
+int sr_tp_peer_handle(void* peer, uint8_t* h_handle64);
+int sr_tp_peer_open(void* peer, const uint8_t* h_handles);   /* world x 64 bytes, rank order */
+int sr_tp_peer_base(void* peer, uint64_t* h_base);
+int sr_tp_peer_attach(void* peer, const uint64_t* h_bases); /* world device pointers */
+int sr_tp_peer_destroy(void* peer);
+int sr_model_set_tp_peer(void* model, void* peer);
+
 /* device timings of the last sr_generate / sr_score on this model */
 int sr_last_timing(void* model, sr_timing* h_out);
 

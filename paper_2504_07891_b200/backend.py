@@ -515,18 +515,67 @@ class NativeEngine:
         return out
 
 
-class TensorParallel:
-    """An NCCL communicator of the C-ABI (``sr_tp_comm_create``) for one rank
-    of a tensor-parallel base model.  ``from_dist`` distributes the 128-byte
-    id over an initialised torch.distributed group (gloo or nccl)."""
+class PeerTransport:
+    """This rank's NVLink peer-memory exchange buffer (``sr_tp_peer_*``): the
+    transport of the fused tensor-parallel decode kernel and of the one-shot
+    prefill / readout collectives.  Ranks connect through CUDA IPC handles
+    (``connect_ipc``, across processes) or plain device pointers
+    (``connect_local``, ranks of one process)."""
 
-    def __init__(self, rank: int, world: int, uid: bytes) -> None:
-        lib = native.load()
+    # mailboxes sized for the bench shapes: d_model <= 8192, 256-row prefill chunks
+    DEC_ROW = 8192
+    MAX_ELEMS = 256 * 8192
+
+    def __init__(self, rank: int, world: int, max_elems: int = MAX_ELEMS,
+                 dec_row: int = DEC_ROW) -> None:
+        self.lib = native.load()
         self.rank, self.world = rank, world
-        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
-        comm = C.c_void_p()
-        native.check("sr_tp_comm_create", lib.sr_tp_comm_create(buf, world, rank, C.byref(comm)))
-        self.comm = comm
+        h = C.c_void_p()
+        native.check("sr_tp_peer_create", self.lib.sr_tp_peer_create(world, rank, max_elems,
+                                                                     dec_row, C.byref(h)))
+        self.handle = h
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        native.check("sr_tp_peer_handle", self.lib.sr_tp_peer_handle(self.handle, buf))
+        return bytes(buf)
+
+    def connect_ipc(self, handles: list[bytes]) -> None:
+        buf = (C.c_uint8 * (64 * self.world)).from_buffer_copy(b"".join(handles))
+        native.check("sr_tp_peer_open", self.lib.sr_tp_peer_open(self.handle, buf))
+
+    def base(self) -> int:
+        v = C.c_uint64()
+        native.check("sr_tp_peer_base", self.lib.sr_tp_peer_base(self.handle, C.byref(v)))
+        return v.value
+
+    def connect_local(self, bases: list[int]) -> None:
+        arr = (C.c_uint64 * self.world)(*bases)
+        native.check("sr_tp_peer_attach", self.lib.sr_tp_peer_attach(self.handle, arr))
+
+    def close(self) -> None:
+        if self.handle is not None and self.handle.value:
+            self.lib.sr_tp_peer_destroy(self.handle)
+            self.handle = None
+
+
+class TensorParallel:
+    """One rank of a tensor-parallel base model (config C4): the rank / world
+    plus its transports -- an NCCL communicator of the C-ABI
+    (``sr_tp_comm_create``), a ``PeerTransport``, or both (then prefill uses
+    NCCL's ring all-reduce and decode the fused peer-memory kernel)."""
+
+    def __init__(self, rank: int, world: int, uid: bytes | None = None,
+                 peer: PeerTransport | None = None) -> None:
+        self.rank, self.world = rank, world
+        self.comm = None
+        self.peer = peer
+        if uid is not None:
+            buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+            comm = C.c_void_p()
+            native.check("sr_tp_comm_create",
+                         native.load().sr_tp_comm_create(buf, world, rank, C.byref(comm)))
+            self.comm = comm
 
     @staticmethod
     def unique_id() -> bytes:
@@ -535,23 +584,47 @@ class TensorParallel:
         return bytes(buf)
 
     @classmethod
-    def from_dist(cls, group=None) -> "TensorParallel":
+    def from_dist(cls, group=None, transport: str = "peer") -> "TensorParallel":
+        """Collective over an initialised torch.distributed group (gloo or
+        nccl): ``transport`` "peer" (NVLink peer memory, IPC handles
+        all-gathered), "nccl", or "both"."""
         import torch.distributed as dist
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
-        box = [cls.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(box, src=0, group=group)
-        return cls(rank, world, box[0])
+        uid = peer = None
+        if transport in ("nccl", "both"):
+            box = [cls.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = box[0]
+        if transport in ("peer", "both"):
+            peer = PeerTransport(rank, world)
+            handles: list = [None] * world
+            dist.all_gather_object(handles, peer.ipc_handle(), group=group)
+            peer.connect_ipc(handles)
+        return cls(rank, world, uid, peer)
 
     @classmethod
     def single(cls) -> "TensorParallel":
-        """World-size-1 communicator: runs every TP code path on one GPU."""
+        """World-size-1 NCCL communicator: runs every TP code path on one GPU."""
         return cls(0, 1, cls.unique_id())
+
+    @classmethod
+    def local_group(cls, world: int) -> list["TensorParallel"]:
+        """``world`` ranks in this process over peer memory (e.g. several
+        ranks sharing one GPU in a test): buffers connected by pointer."""
+        peers = [PeerTransport(r, world) for r in range(world)]
+        bases = [p.base() for p in peers]
+        for p in peers:
+            p.connect_local(bases)
+        return [cls(r, world, None, peers[r]) for r in range(world)]
 
     def close(self) -> None:
         if self.comm is not None and self.comm.value:
             native.load().sr_tp_comm_destroy(self.comm)
             self.comm = None
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
 
 
 class B200Backend(ModelBackend):
@@ -581,8 +654,11 @@ class B200Backend(ModelBackend):
         pages_per_stream = math.ceil(max_pos / PAGE) + 1
         model = DeviceModel(spec, weights, max_pos=max_pos, n_pages=n_streams * pages_per_stream,
                             max_tokens=max_tokens, max_new=max_new, device=device)
-        if tp is not None:
+        if tp is not None and tp.comm is not None:
             native.check("sr_model_set_tp", model.lib.sr_model_set_tp(model.handle, tp.comm))
+        if tp is not None and tp.peer is not None:
+            native.check("sr_model_set_tp_peer",
+                         model.lib.sr_model_set_tp_peer(model.handle, tp.peer.handle))
         self.tp = tp
         vocab = vocab or shared_vocab(spec.vocab_text)
         T = types

@@ -109,6 +109,27 @@ SR_DEV void warp_top2(Top2& t) {
   }
 }
 
+// --------------------------------------------- system-scope flag helpers ---
+// (peer-memory collectives, tp.cu / decode_mk.cu): arrivals are release adds
+// on a rank's flag word, waits acquire-poll the local flag
+SR_DEV unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+SR_DEV void red_release_sys(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+SR_DEV void peer_wait(const unsigned* flag, unsigned target) {
+  const long long t0 = clock64();
+  for (unsigned spin = 0;; ++spin) {
+    if ((int)(ld_acquire_sys(flag) - target) >= 0) return;
+    if ((spin & 4095) == 4095 && clock64() - t0 > 20000000000ll) __trap();  // ~10 s: a peer died
+  }
+}
+
 // ------------------------------------------------------- layout helpers ---
 // K/V pool: [layer][page][kv_head][SR_PAGE][128] bf16
 SR_DEV size_t kv_offset(int layer, int page, int kvh, int slot, int n_pages, int n_kv) {

@@ -211,10 +211,13 @@ SR_DEV void mk_grid_sync(unsigned* ctr, unsigned& target, int G, int sleep_ns) {
 // weight, up to four partials per row) is issued before any is used, so a
 // batch costs one round trip; h and w wait in shared memory (`tmp`, the idle
 // K/V page buffer) for the block-wide sum of squares.
+// With tensor parallelism (`mb` non-null, mode 1) the update is instead the
+// all-ranks sum read from this rank's decode mailbox: h = hin + sum over
+// ranks q = 0..W-1 (in rank order) of mb[q][i].
 SR_DEV void mk_norm_prologue(const MkParams& p, int mode, int tok, const float* hin,
                              const float* part, const uint16_t* tab, const __nv_bfloat16* w,
                              float* hout, __nv_bfloat16* xs, float* red, int c, int G,
-                             float* tmp) {
+                             float* tmp, const float* mb = nullptr) {
   const int d = p.d, tid = threadIdx.x;
   float* hs = tmp;                                            // [d] fp32
   __nv_bfloat16* wsm = reinterpret_cast<__nv_bfloat16*>(tmp + d);  // [d] bf16
@@ -236,6 +239,18 @@ SR_DEV void mk_norm_prologue(const MkParams& p, int mode, int tok, const float* 
         hb[jj] = bf_to_f(p.embed[(size_t)tok * d + ic]);
         nb[jj] = 0;
         pb[jj][0] = pb[jj][1] = pb[jj][2] = pb[jj][3] = 0.f;
+      } else if (mb) {  // tensor parallel: the ranks' deltas, summed in rank order
+        hb[jj] = __ldcg(hin + ic);
+        float r[kPeerMaxWorld];
+#pragma unroll
+        for (int q = 0; q < kPeerMaxWorld; ++q)
+          r[q] = q < p.tp_world ? __ldcg(mb + (size_t)q * p.tp_dec_row + ic) : 0.f;
+        float sp = r[0];
+#pragma unroll
+        for (int q = 1; q < kPeerMaxWorld; ++q) sp += r[q];
+        pb[jj][0] = sp;
+        pb[jj][1] = pb[jj][2] = pb[jj][3] = 0.f;
+        nb[jj] = 1;
       } else {
         hb[jj] = __ldcg(hin + ic);
         const int e = tab[ic / kTR];
@@ -289,6 +304,69 @@ SR_DEV void mk_stage_vec(const __nv_bfloat16* src, int K, __nv_bfloat16* xs) {
   }
   for (int i = K + threadIdx.x; i < Kp; i += kMkConsumers) xs[i] = __float2bfloat16_rn(0.f);
   cbar();
+}
+
+// Tensor parallelism: after a row-parallel phase (O, down) and its grid
+// barrier, CTA c sums this rank's split partials of rows [c*d/G, (c+1)*d/G)
+// (the rank's delta) and stores them into slot [rank] of every rank's decode
+// mailbox over NVLink; thread 0 then release-adds every rank's flag and
+// acquires its own until all W*G arrivals of this exchange are in.  Returns
+// this rank's mailbox slot, which the next prologue sums in rank order.
+SR_DEV const float* mk_tp_exchange(const MkParams& p, const float* part, const uint16_t* tab,
+                                   unsigned& ex, int c, int G) {
+  const int slot = (int)(ex & 1u);
+  const unsigned target = (ex / 2 + 1) * (unsigned)(p.tp_world * G);
+  ex += 1;
+  const size_t soff = p.tp_off_dec + (size_t)slot * p.tp_world * p.tp_dec_row * 4;
+  const int r0 = (int)((long long)p.d * c / G), r1 = (int)((long long)p.d * (c + 1) / G);
+  for (int i = r0 + (int)threadIdx.x; i < r1; i += kMkConsumers) {
+    const float v = mk_sum_parts(part, tab, i, p.maxj);
+    for (int q = 0; q < p.tp_world; ++q)
+      reinterpret_cast<float*>(p.tp_base[q] + soff)[(size_t)p.tp_rank * p.tp_dec_row + i] = v;
+  }
+  cbar();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < p.tp_world; ++q)
+      red_release_sys(reinterpret_cast<unsigned*>(p.tp_base[q]) + 2 + slot, 1u);
+    peer_wait(reinterpret_cast<const unsigned*>(p.tp_base[p.tp_rank]) + 2 + slot, target);
+  }
+  cbar();
+  return reinterpret_cast<const float*>(p.tp_base[p.tp_rank] + soff);
+}
+
+// Tensor parallelism: the vocab-parallel greedy merge.  Every CTA holds this
+// rank's (top-1, global index, top-2); CTA 0 stores it into slot [rank] of
+// every rank's greedy mailbox; all CTAs wait for the W entries and merge them
+// in rank order (ties -> lower id), so every rank picks the same token.
+SR_DEV Top2 mk_tp_merge(const MkParams& p, Top2 mine, unsigned& lx, int c) {
+  const int slot = (int)(lx & 1u);
+  const unsigned target = (lx / 2 + 1) * (unsigned)p.tp_world;
+  lx += 1;
+  const size_t soff = p.tp_off_lm + (size_t)slot * p.tp_world * 4 * 4;
+  if (c == 0 && threadIdx.x == 0) {
+    for (int q = 0; q < p.tp_world; ++q) {
+      float* dst = reinterpret_cast<float*>(p.tp_base[q] + soff) + p.tp_rank * 4;
+      dst[0] = mine.v1;
+      dst[1] = __int_as_float(mine.i1);
+      dst[2] = mine.v2;
+    }
+    __threadfence_system();
+    for (int q = 0; q < p.tp_world; ++q)
+      red_release_sys(reinterpret_cast<unsigned*>(p.tp_base[q]) + 4 + slot, 1u);
+  }
+  __shared__ float s_m[kPeerMaxWorld * 4];
+  if (threadIdx.x == 0) {
+    peer_wait(reinterpret_cast<const unsigned*>(p.tp_base[p.tp_rank]) + 4 + slot, target);
+    const float* mb = reinterpret_cast<const float*>(p.tp_base[p.tp_rank] + soff);
+    for (int i = 0; i < 4 * p.tp_world; ++i) s_m[i] = __ldcg(mb + i);
+  }
+  cbar();
+  Top2 b;
+  b.init();
+  for (int q = 0; q < p.tp_world; ++q) b.merge(s_m[4 * q], __float_as_int(s_m[4 * q + 1]), s_m[4 * q + 2]);
+  cbar();
+  return b;
 }
 
 // ring position shared by the consumer warps (every warp walks every stage)
@@ -737,7 +815,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   __shared__ uint16_t s_tab[3][kMkTab];  // contributor tables: qkv, o, down
   __shared__ PhaseInfo s_ph[5];
   __shared__ __align__(8) uint64_t kvbar;
-  __shared__ float s_margin;
+  __shared__ float s_margin, s_rv1, s_rv2;
   __shared__ volatile int s_stop;
 
   const int S = p.stages;
@@ -840,6 +918,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   const int Gq = p.H / p.KV;
   (void)Gq;
   bool done = st->done != 0;
+  // tensor parallelism: exchange counters continue across launches (words 8-9
+  // of this rank's buffer; every rank runs the same exchange sequence)
+  const bool tp = p.tp_world > 1;
+  unsigned* tp_ctr = tp ? reinterpret_cast<unsigned*>(p.tp_base[p.tp_rank]) + 8 : nullptr;
+  unsigned ex = tp ? tp_ctr[0] : 0u, lx = tp ? tp_ctr[1] : 0u;
+  const float* mb_d = nullptr;  // mailbox slot of the last down exchange
   // SR_MK_PROF: CTA 0 records a globaltimer stamp after every step of the
   // first decoded token (sr_debug_profile)
   const bool prof = p.prof != nullptr && c == 0 && threadIdx.x == 0;
@@ -878,7 +962,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       if (l == 0)
         mk_norm_prologue(p, 0, tok, nullptr, nullptr, s_tab[2], ly.ln1, p.hA, xs, red, c, G, kvtmp);
       else
-        mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], ly.ln1, p.hA, xs, red, c, G, kvtmp);
+        mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], ly.ln1, p.hA, xs, red, c, G, kvtmp,
+                         mb_d);
       MK_EV();  // 1 qkv prologue
       mk_gemv<PH_QKV>(p, s_ph[PH_QKV], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 2 qkv gemv
@@ -909,8 +994,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       MK_EV();  // 9 o gemv
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 10 sync
+      const float* mb_o = tp ? mk_tp_exchange(p, p.part_o, s_tab[1], ex, c, G) : nullptr;
       // gate / up
-      mk_norm_prologue(p, 1, tok, p.hA, p.part_o, s_tab[1], ly.ln2, p.hB, xs, red, c, G, kvtmp);
+      mk_norm_prologue(p, 1, tok, p.hA, p.part_o, s_tab[1], ly.ln2, p.hB, xs, red, c, G, kvtmp,
+                       mb_o);
       MK_EV();  // 11 prologue
       mk_gemv<PH_GU>(p, s_ph[PH_GU], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 12 gu gemv
@@ -923,9 +1010,11 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       MK_EV();  // 15 down gemv
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 16 sync
+      if (tp) mb_d = mk_tp_exchange(p, p.part_d, s_tab[2], ex, c, G);
     }
     // LM head + greedy argmax
-    mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], p.ln_f, nullptr, xs, red, c, G, kvtmp);
+    mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], p.ln_f, nullptr, xs, red, c, G, kvtmp,
+                     mb_d);
     MK_EV();
     mk_gemv<PH_LM>(p, s_ph[PH_LM], c, ring, full, empty, xs, rp, S, best);
     MK_EV();
@@ -954,10 +1043,24 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       warp_top2(b);
       if (lane == 0) {
         s_tok = b.i1;
+        s_rv1 = b.v1;
+        s_rv2 = b.v2;
         s_margin = b.v1 - b.v2;
       }
     }
     cbar();
+    if (tp) {  // this rank's vocab shard -> global greedy choice over all ranks
+      Top2 mine;
+      mine.v1 = s_rv1;
+      mine.v2 = s_rv2;
+      mine.i1 = s_tok + p.vocab_base;
+      const Top2 b = mk_tp_merge(p, mine, lx, c);
+      if (threadIdx.x == 0) {
+        s_tok = b.i1;
+        s_margin = b.v1 - b.v2;
+      }
+      cbar();
+    }
     const int t = s_tok;
     const int cls = token_class[t];
     int finish = SR_FINISH_LENGTH;
@@ -992,6 +1095,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
     if (prof) ev = kMkProfEvents;  // first token only
   }
 #undef MK_EV
+  if (tp && c == 0 && threadIdx.x == 0) {
+    tp_ctr[0] = ex;
+    tp_ctr[1] = lx;
+  }
   if (threadIdx.x == 0) s_stop = 1;
 }
 

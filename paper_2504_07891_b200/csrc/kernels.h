@@ -206,6 +206,8 @@ struct MkLayer {
   const void* pad;
 };
 
+constexpr int kPeerMaxWorld = 8;  // ranks of a peer-memory TP group
+
 struct MkParams {
   const CUtensorMap* maps;   // device [L*4 + 1]: per layer qkv, o, gate/up, down; then LM head
   const MkLayer* layers;     // device [L]
@@ -237,6 +239,11 @@ struct MkParams {
   int bar_sleep;             // ns of backoff between grid-barrier polls
   int evict_first;           // stream weights with an L2 evict-first policy
   int min_pages;             // attention: minimum K/V pages per split
+  // tensor parallelism over NVLink peer memory (tp_world > 1): every rank's
+  // exchange buffer (flags at the head, tp.cu), the decode / greedy mailboxes
+  int tp_world, tp_rank, vocab_base, tp_dec_row;
+  char* tp_base[kPeerMaxWorld];
+  size_t tp_off_dec, tp_off_lm;
 };
 
 size_t mk_smem_bytes(int stages, int xs_elems);
@@ -245,6 +252,23 @@ int mk_max_j(int N, int K, int num_sms);
 int mk_tile_rows();
 int mk_tile_cols();
 cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream);
+
+// NVLink peer-memory transport (tp.cu): one exchange buffer per rank
+struct PeerComm {
+  int world, rank;
+  int dec_row;                       // floats per rank row of the decode mailbox (>= d_model)
+  size_t max_elems;                  // floats per rank of the host-collective mailbox
+  size_t off_dec, off_lm, off_big, bytes;
+  char* local;                       // this rank's buffer (cudaMalloc)
+  char* base[kPeerMaxWorld];         // every rank's buffer in this device's address space
+  bool opened[kPeerMaxWorld];        // opened through cudaIpcOpenMemHandle
+  unsigned seq;                      // host-driven exchanges issued so far
+};
+void peer_layout(PeerComm* pc);
+// mode 0: all-reduce sum f32, 1: all-gather f32 (recv [world][n]), 2: broadcast
+// from root, 3: all-reduce sum i32; returns 0, or < 0 on a launch / size error
+int peer_exchange(PeerComm* pc, int mode, const float* send, float* recv, size_t n, int root,
+                  cudaStream_t s);
 
 // tensor parallelism (tp.cu)
 int tp_available();

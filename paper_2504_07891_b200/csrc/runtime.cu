@@ -48,19 +48,20 @@ struct Layout {  // workspace carve-up (byte offsets)
       mk_maps, mk_layers, mk_h, mk_part, mk_apart, mk_lm, mk_prof, mk_ctab, tp_delta, tp_small, attn_items, attn_tabs,
       total;
   int mk_maxj;
+  int mk_g;  // CTAs of the persistent decode kernel
   int nsplit_decode;
   size_t part_floats;
 };
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
-// CTAs of the persistent decode kernel: one per SM unless SR_MK_CTAS asks for
-// fewer (an experiment knob: fewer CTAs arrive at each grid barrier)
+// CTAs of the persistent decode kernel: one per SM unless SR_MK_CTAS (read
+// when the model's workspace is sized and created) asks for fewer -- an
+// experiment knob, and how tensor-parallel ranks sharing one GPU in a test
+// leave each other room to be co-resident
 static int mk_ctas_for(int num_sms) {
-  static const int v = [] {
-    const char* e = getenv("SR_MK_CTAS");
-    return e ? atoi(e) : 0;
-  }();
+  const char* e = getenv("SR_MK_CTAS");
+  const int v = e ? atoi(e) : 0;
   return v >= 16 && v < num_sms ? v : num_sms;
 }
 
@@ -95,6 +96,7 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
   L.ro_cnt = take(64);
   // persistent decode kernel (decode_mk.cu)
   const int mk_g = mk_ctas_for(num_sms);
+  L.mk_g = mk_g;
   const int qd_i = d.n_heads * SR_HEAD_DIM, qkv_i = qd_i + 2 * d.n_kv_heads * SR_HEAD_DIM;
   L.mk_maxj = std::max({mk_max_j(qkv_i, d.d_model, mk_g), mk_max_j(d.d_model, qd_i, mk_g),
                         mk_max_j(d.d_model, d.d_ffn, mk_g)});
@@ -143,7 +145,9 @@ struct Model {
   bool graph_decode = false;   // SR_DECODE=graph: per-kernel decode graph (A/B reference)
   MkParams mk{};
   int* trace_host = nullptr;
-  void* tp_comm = nullptr;  // sr_model_set_tp; non-null: the TP code paths run
+  void* tp_comm = nullptr;  // sr_model_set_tp (NCCL); non-null: the TP code paths run
+  PeerComm* tp_peer = nullptr;  // sr_model_set_tp_peer (NVLink peer memory)
+  bool tp_on() const { return tp_comm || tp_peer; }
   float* tp_delta = nullptr;
   float *tp_send, *tp_gather, *tp_dig, *tp_dec;
   int* tp_counts;
@@ -206,7 +210,7 @@ struct Model {
       const int N3[3] = {qkv_rows, d.d_model, d.d_model};
       const int K3[3] = {d.d_model, q_dim, d.d_ffn};
       std::vector<uint16_t> tab(3 * 256, 0);
-      const long G = mk_ctas_for(num_sms);
+      const long G = L.mk_g;
       if (G > 255) return fail(SR_E_INVALID, "decode tables assume <= 255 SMs");
       for (int t = 0; t < 3; ++t) {
         const int tcol = std::min(K3[t], mk_tile_cols());
@@ -243,7 +247,7 @@ struct Model {
     p.v_pool = v_pool;
     p.hA = at<float>(L.mk_h);
     p.hB = p.hA + d.d_model;
-    const size_t pstride = (size_t)mk_ctas_for(num_sms) * L.mk_maxj * mk_tile_rows();
+    const size_t pstride = (size_t)L.mk_g * L.mk_maxj * mk_tile_rows();
     p.part_qkv = at<float>(L.mk_part);
     p.part_o = p.part_qkv + pstride;
     p.part_d = p.part_o + pstride;
@@ -556,7 +560,7 @@ struct Model {
       if (rc) return -rc;
       ep = epi_base(M, d.d_model);
       ep.norm_w = lw(l, LN2);
-      if (tp_comm)
+      if (tp_on())
         if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
       SR_CK(epi_resid_norm_launch(ep, s));
       // gate/up
@@ -572,7 +576,7 @@ struct Model {
       if (rc) return -rc;
       ep = epi_base(M, d.d_model);
       ep.norm_w = (l + 1 < d.n_layers) ? lw(l + 1, LN1) : ln_f;
-      if (tp_comm)
+      if (tp_on())
         if (int rc2 = tp_reduce_rows(ep, M, s)) return -rc2;
       SR_CK(epi_resid_norm_launch(ep, s));
     }
@@ -585,12 +589,37 @@ struct Model {
     return 0;
   }
 
+  // host-driven collectives: NCCL when a communicator is attached (ring
+  // algorithms for the large prefill deltas), else the peer-memory one-shot
+  int peer_check(int r, const char* what) {
+    if (r != 0) return fail(SR_E_TP, std::string(what) + ": peer exchange failed (" +
+                                         std::to_string(r) + ")");
+    return 0;
+  }
+  int coll_all_reduce_f32(float* buf, size_t n, cudaStream_t s) {
+    if (tp_comm) return tp_check(tp_all_reduce_f32(tp_comm, buf, n, s), "ncclAllReduce");
+    return peer_check(peer_exchange(tp_peer, 0, buf, buf, n, 0, s), "all-reduce");
+  }
+  int coll_all_reduce_i32(int* buf, size_t n, cudaStream_t s) {
+    if (tp_comm) return tp_check(tp_all_reduce_i32(tp_comm, buf, n, s), "ncclAllReduce");
+    return peer_check(peer_exchange(tp_peer, 3, reinterpret_cast<float*>(buf),
+                                    reinterpret_cast<float*>(buf), n, 0, s), "all-reduce");
+  }
+  int coll_all_gather_f32(const float* send, float* recv, size_t n, cudaStream_t s) {
+    if (tp_comm) return tp_check(tp_all_gather_f32(tp_comm, send, recv, n, s), "ncclAllGather");
+    return peer_check(peer_exchange(tp_peer, 1, send, recv, n, 0, s), "all-gather");
+  }
+  int coll_broadcast_f32(const float* send, float* recv, size_t n, int root, cudaStream_t s) {
+    if (tp_comm) return tp_check(tp_broadcast_f32(tp_comm, send, recv, n, root, s), "ncclBroadcast");
+    return peer_check(peer_exchange(tp_peer, 2, send, recv, n, root, s), "broadcast");
+  }
+
   // prefill: all-reduce the row-parallel output (split partials -> delta)
   // and point the residual epilogue at it
   int tp_reduce_rows(EpiParams& ep, int M, cudaStream_t s) {
     const size_t n = (size_t)M * d.d_model;
     SR_CK(split_sum_launch(part, ep.splits, (size_t)M * d.d_model, tp_delta, n, s));
-    if (int rc = tp_check(tp_all_reduce_f32(tp_comm, tp_delta, n, s), "ncclAllReduce")) return rc;
+    if (int rc = coll_all_reduce_f32(tp_delta, n, s)) return rc;
     ep.part = tp_delta;
     ep.splits = 1;
     return 0;
@@ -601,8 +630,7 @@ struct Model {
     const int grid = std::min(gemv_max_grid(num_sms), (d.vocab_text + 255) / 256);
     SR_CK(tp_top2_local_launch(logits, d.vocab_text, d.vocab_base, lm_v1, lm_v2, lm_i1, lm_ctr,
                                tp_send, std::max(grid, 1), s));
-    if (int rc = tp_check(tp_all_gather_f32(tp_comm, tp_send, tp_gather, 3, s), "ncclAllGather"))
-      return rc;
+    if (int rc = coll_all_gather_f32(tp_send, tp_gather, 3, s)) return rc;
     SR_CK(tp_select_launch(tp_gather, d.tp_world, st, s));
     return 0;
   }
@@ -899,7 +927,7 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
   if (!m || !page_table || !ids || !token_class || !out) return fail(SR_E_INVALID, "null argument");
   if (n_ids < 1 || max_new < 1 || start_pos < 0) return fail(SR_E_INVALID, "bad sizes");
   if (max_new > m->d.max_new) return fail(SR_E_CAPACITY, "max_new exceeds the model's max_new");
-  if (m->d.tp_world > 1 && !m->tp_comm) return fail(SR_E_INVALID, "tensor-parallel model without a communicator");
+  if (m->d.tp_world > 1 && !m->tp_on()) return fail(SR_E_INVALID, "tensor-parallel model without a communicator");
   if (start_pos + n_ids + max_new > m->d.max_pos)
     return fail(SR_E_CAPACITY, "positions exceed max_pos");
   cudaStream_t s = (cudaStream_t)stream;
@@ -929,7 +957,7 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
   p.part_v2 = m->lm_v2;
   p.part_i1 = m->lm_i1;
   p.counter = m->lm_ctr;
-  if (m->tp_comm) {  // vocab-parallel first choice
+  if (m->tp_on()) {  // vocab-parallel first choice
     p.logits = m->logits;
     SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
     if (int rc2 = m->tp_select(s)) return rc2;
@@ -937,7 +965,11 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
     SR_CK(gemv_launch(GEMV_LM_ARGMAX_X, p, m->num_sms, s, false));
   }
   SR_CK(cudaEventRecord(m->ev[1], s));
-  if (m->tp_comm) {
+  if (m->tp_peer) {
+    // tensor parallel over peer memory: the persistent kernel decodes the
+    // step, exchanging the row-parallel deltas and the greedy merge in-kernel
+    SR_CK(mk_launch(m->mk, m->L.mk_g, s));
+  } else if (m->tp_comm) {
     // host-driven token loop: the exchanges are NCCL calls between kernels
     for (int i = 0; i < max_new; ++i) {
       int done = 0;
@@ -948,7 +980,7 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
     }
   } else if (!m->stream_decode && !m->graph_decode) {
     // one persistent kernel decodes the whole step (decode_mk.cu)
-    SR_CK(mk_launch(m->mk, mk_ctas_for(m->num_sms), s));
+    SR_CK(mk_launch(m->mk, m->L.mk_g, s));
   } else if (m->graph_decode) {
     SR_CK(cudaGraphLaunch(m->exec, s));
   } else {
@@ -976,7 +1008,7 @@ int sr_score(void* model, const int32_t* page_table, int32_t start_pos, const in
   if (!m || !page_table || !ids || !first_digit || !readout) return fail(SR_E_INVALID, "null argument");
   if (n_ids < 1 || start_pos < 0) return fail(SR_E_INVALID, "bad sizes");
   if (start_pos + n_ids > m->d.max_pos) return fail(SR_E_CAPACITY, "positions exceed max_pos");
-  if (m->d.tp_world > 1 && !m->tp_comm) return fail(SR_E_INVALID, "tensor-parallel model without a communicator");
+  if (m->d.tp_world > 1 && !m->tp_on()) return fail(SR_E_INVALID, "tensor-parallel model without a communicator");
   cudaStream_t s = (cudaStream_t)stream;
   SR_CK(cudaEventRecord(m->ev[0], s));
   int rows = 0;
@@ -990,21 +1022,16 @@ int sr_score(void* model, const int32_t* page_table, int32_t start_pos, const in
   p.x = m->x + (size_t)(rows - 1) * m->d.d_model;
   p.logits = m->logits;
   SR_CK(gemv_launch(GEMV_LM_LOGITS_X, p, m->num_sms, s, false));
-  if (m->tp_comm) {
+  if (m->tp_on()) {
     // digits 0-9 are rows of rank 0's shard: broadcast their logits, count
     // ranks locally, all-reduce the counts, all-gather the local top-2s
-    if (int rc2 = m->tp_check(tp_broadcast_f32(m->tp_comm, m->logits, m->tp_dig, 10, 0, s),
-                              "ncclBroadcast"))
-      return rc2;
+    if (int rc2 = m->coll_broadcast_f32(m->logits, m->tp_dig, 10, 0, s)) return rc2;
     const int grid = std::max(1, std::min(m->num_sms, (m->d.vocab_text + 255) / 256));
     SR_CK(tp_readout_local_launch(m->logits, m->d.vocab_text, m->d.vocab_base, m->tp_dig,
                                   m->tp_counts, m->lm_v1, m->lm_v2, m->lm_i1, m->lm_ctr,
                                   m->tp_send, grid, s));
-    if (int rc2 = m->tp_check(tp_all_reduce_i32(m->tp_comm, m->tp_counts, 10, s), "ncclAllReduce"))
-      return rc2;
-    if (int rc2 = m->tp_check(tp_all_gather_f32(m->tp_comm, m->tp_send, m->tp_gather, 3, s),
-                              "ncclAllGather"))
-      return rc2;
+    if (int rc2 = m->coll_all_reduce_i32(m->tp_counts, 10, s)) return rc2;
+    if (int rc2 = m->coll_all_gather_f32(m->tp_send, m->tp_gather, 3, s)) return rc2;
     SR_CK(tp_readout_final_launch(m->tp_dig, m->tp_counts, m->tp_gather, m->d.tp_world,
                                   first_digit, threshold, readout, s));
     SR_CK(cudaEventRecord(m->ev[1], s));
@@ -1077,7 +1104,7 @@ int sr_verify_tokens(void* model, const int32_t* page_table, int32_t start_pos,
   if (n_ids < 1 || start_pos < 0 || start_pos + n_ids > m->d.max_pos)
     return fail(SR_E_INVALID, "bad sizes");
   if (n_ids > m->d.max_tokens) return fail(SR_E_CAPACITY, "n_ids exceeds max_tokens");
-  if (m->tp_comm) return fail(SR_E_INVALID, "sr_verify_tokens: tensor parallelism not supported");
+  if (m->tp_on()) return fail(SR_E_INVALID, "sr_verify_tokens: tensor parallelism not supported");
   cudaStream_t s = (cudaStream_t)stream;
   SR_CK(cudaEventRecord(m->ev[0], s));
   int rows = 0;
@@ -1111,7 +1138,7 @@ static int batch_spans(Model* m, int32_t n_seq, const int32_t* const* page_table
                        std::vector<Model::SeqSpan>& spans, int* total) {
   if (n_seq < 1 || n_seq > kMaxSeqs) return fail(SR_E_INVALID, "n_seq out of range");
   if (!page_tables || !start_pos || !n_ids) return fail(SR_E_INVALID, "null argument");
-  if (m->tp_comm || m->d.tp_world > 1)
+  if (m->tp_on() || m->d.tp_world > 1)
     return fail(SR_E_INVALID, "batched calls: tensor parallelism not supported");
   spans.resize(n_seq);
   int row = 0;
@@ -1232,6 +1259,111 @@ int sr_model_set_tp(void* model, void* comm) {
   if (!m) return fail(SR_E_INVALID, "null model");
   if (m->d.tp_world > 1 && !comm) return fail(SR_E_INVALID, "tp_world > 1 needs a communicator");
   m->tp_comm = comm;
+  return 0;
+}
+
+// ----------------------------------------------- peer-memory TP transport ---
+int sr_tp_peer_create(int32_t world, int32_t rank, int64_t max_elems, int32_t dec_row,
+                      void** out_peer) {
+  if (!out_peer || world < 1 || world > kPeerMaxWorld || rank < 0 || rank >= world ||
+      max_elems < 16 || dec_row < 1)
+    return fail(SR_E_INVALID, "bad peer transport arguments");
+  PeerComm* pc = new PeerComm{};
+  pc->world = world;
+  pc->rank = rank;
+  pc->max_elems = (size_t)max_elems;
+  pc->dec_row = (dec_row + 63) / 64 * 64;
+  peer_layout(pc);
+  cudaError_t e = cudaMalloc((void**)&pc->local, pc->bytes);
+  if (e == cudaSuccess) e = cudaMemset(pc->local, 0, pc->bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (pc->local) cudaFree(pc->local);
+    delete pc;
+    return fail(e, std::string("peer buffer: ") + cudaGetErrorString(e));
+  }
+  pc->base[rank] = pc->local;
+  *out_peer = pc;
+  return 0;
+}
+
+int sr_tp_peer_handle(void* peer, uint8_t* h_handle64) {
+  PeerComm* pc = (PeerComm*)peer;
+  if (!pc || !h_handle64) return fail(SR_E_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  SR_CK(cudaIpcGetMemHandle(&h, pc->local));
+  memcpy(h_handle64, &h, sizeof(h));
+  return 0;
+}
+
+int sr_tp_peer_open(void* peer, const uint8_t* h_handles) {
+  PeerComm* pc = (PeerComm*)peer;
+  if (!pc || !h_handles) return fail(SR_E_INVALID, "null argument");
+  for (int q = 0; q < pc->world; ++q) {
+    if (q == pc->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, h_handles + (size_t)q * sizeof(h), sizeof(h));
+    void* ptr = nullptr;
+    SR_CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    pc->base[q] = (char*)ptr;
+    pc->opened[q] = true;
+  }
+  return 0;
+}
+
+int sr_tp_peer_base(void* peer, uint64_t* h_base) {
+  PeerComm* pc = (PeerComm*)peer;
+  if (!pc || !h_base) return fail(SR_E_INVALID, "null argument");
+  *h_base = (uint64_t)(uintptr_t)pc->local;
+  return 0;
+}
+
+int sr_tp_peer_attach(void* peer, const uint64_t* h_bases) {
+  PeerComm* pc = (PeerComm*)peer;
+  if (!pc || !h_bases) return fail(SR_E_INVALID, "null argument");
+  for (int q = 0; q < pc->world; ++q) {
+    if (q == pc->rank) continue;
+    if (!h_bases[q]) return fail(SR_E_INVALID, "null peer buffer");
+    pc->base[q] = (char*)(uintptr_t)h_bases[q];
+  }
+  return 0;
+}
+
+int sr_tp_peer_destroy(void* peer) {
+  PeerComm* pc = (PeerComm*)peer;
+  if (!pc) return 0;
+  for (int q = 0; q < pc->world; ++q)
+    if (pc->opened[q]) cudaIpcCloseMemHandle(pc->base[q]);
+  if (pc->local) cudaFree(pc->local);
+  delete pc;
+  return 0;
+}
+
+int sr_model_set_tp_peer(void* model, void* peer) {
+  Model* m = (Model*)model;
+  if (!m) return fail(SR_E_INVALID, "null model");
+  PeerComm* pc = (PeerComm*)peer;
+  if (!pc) {
+    if (m->d.tp_world > 1 && !m->tp_comm) return fail(SR_E_INVALID, "tp_world > 1 needs a transport");
+    m->tp_peer = nullptr;
+    m->mk.tp_world = 1;
+    return 0;
+  }
+  if (pc->world != m->d.tp_world || pc->rank != m->d.tp_rank)
+    return fail(SR_E_INVALID, "peer transport world / rank differ from the model's");
+  if (pc->dec_row < m->d.d_model || pc->max_elems < (size_t)m->d.max_tokens * m->d.d_model)
+    return fail(SR_E_CAPACITY, "peer transport mailboxes smaller than the model needs");
+  for (int q = 0; q < pc->world; ++q)
+    if (!pc->base[q]) return fail(SR_E_INVALID, "peer transport not connected (open / attach)");
+  m->tp_peer = pc;
+  MkParams& p = m->mk;
+  p.tp_world = pc->world;
+  p.tp_rank = pc->rank;
+  p.vocab_base = m->d.vocab_base;
+  p.tp_dec_row = pc->dec_row;
+  for (int q = 0; q < kPeerMaxWorld; ++q) p.tp_base[q] = q < pc->world ? pc->base[q] : nullptr;
+  p.tp_off_dec = pc->off_dec;
+  p.tp_off_lm = pc->off_lm;
   return 0;
 }
 

@@ -322,4 +322,107 @@ cudaError_t tp_readout_final_launch(const float* dig, int* counts, const float* 
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------- peer transport ---
+// NVLink peer-memory collectives, no NCCL: every rank owns one exchange
+// buffer (cudaMalloc, shared with the other ranks by CUDA IPC handles or, for
+// ranks of one process, by plain device pointers).  A collective is one-shot:
+// each rank stores its contribution into slot [rank] of every rank's mailbox
+// (P2P stores over NVLink), then release-adds every rank's arrival flag; a
+// rank reads only its own buffer, after acquiring its flag.  Sums run over
+// ranks in rank order, so every rank computes bit-identical results.  Two
+// mailbox slots alternate per channel: a rank writes slot s of exchange e+2
+// only after exchange e+1 completed everywhere, i.e. after every rank read
+// slot s of exchange e.
+//
+// Channels (flag words at the head of the buffer): host-driven collectives
+// (prefill deltas, the first token's choice, judge readout) on flags 0-1;
+// the persistent decode kernel's residual exchanges on flags 2-3 and its
+// greedy merge on flags 4-5 (decode_mk.cu); words 8-9 count the kernel's
+// exchanges across launches.
+constexpr int kPeerBlocks = 16;
+constexpr int kPeerThreads = 512;
+
+static size_t peer_align(size_t v) { return (v + 255) & ~size_t(255); }
+
+void peer_layout(PeerComm* pc) {
+  size_t o = 256;  // flags + counters
+  pc->off_dec = o;
+  o = peer_align(o + (size_t)2 * pc->world * pc->dec_row * 4);
+  pc->off_lm = o;
+  o = peer_align(o + (size_t)2 * pc->world * 4 * 4);
+  pc->off_big = o;
+  o = peer_align(o + (size_t)2 * pc->world * pc->max_elems * 4);
+  pc->bytes = o;
+}
+
+struct PeerX {
+  char* base[kPeerMaxWorld];
+  int world, rank, mode, root, slot;
+  size_t off, max_elems, n;
+  unsigned target;
+  const float* send;
+  float* recv;
+};
+
+// mode 0: all-reduce sum (f32), 1: all-gather (f32), 2: broadcast from root,
+// 3: all-reduce sum (i32 bits)
+__global__ void __launch_bounds__(kPeerThreads) peer_exchange_kernel(const PeerX x) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t slot_off = x.off + ((size_t)x.slot * x.world) * x.max_elems * 4;
+  if (x.mode != 2 || x.rank == x.root) {
+    for (size_t i = i0; i < x.n; i += stride) {
+      const float v = x.send[i];
+      for (int q = 0; q < x.world; ++q)
+        reinterpret_cast<float*>(x.base[q] + slot_off)[(size_t)x.rank * x.max_elems + i] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < x.world; ++q)
+      red_release_sys(reinterpret_cast<unsigned*>(x.base[q]) + x.slot, 1u);
+    peer_wait(reinterpret_cast<const unsigned*>(x.base[x.rank]) + x.slot, x.target);
+  }
+  __syncthreads();
+  const float* mb = reinterpret_cast<const float*>(x.base[x.rank] + slot_off);
+  for (size_t i = i0; i < x.n; i += stride) {
+    if (x.mode == 0) {
+      float v = 0.f;
+      for (int q = 0; q < x.world; ++q) v += __ldcg(mb + (size_t)q * x.max_elems + i);
+      x.recv[i] = v;
+    } else if (x.mode == 1) {
+      for (int q = 0; q < x.world; ++q) x.recv[(size_t)q * x.n + i] = __ldcg(mb + (size_t)q * x.max_elems + i);
+    } else if (x.mode == 2) {
+      x.recv[i] = __ldcg(mb + (size_t)x.root * x.max_elems + i);
+    } else {
+      int v = 0;
+      for (int q = 0; q < x.world; ++q) v += __float_as_int(__ldcg(mb + (size_t)q * x.max_elems + i));
+      x.recv[i] = __int_as_float(v);
+    }
+  }
+}
+
+int peer_exchange(PeerComm* pc, int mode, const float* send, float* recv, size_t n, int root,
+                  cudaStream_t s) {
+  if (n > pc->max_elems) return -2;
+  PeerX x{};
+  for (int q = 0; q < pc->world; ++q) x.base[q] = pc->base[q];
+  x.world = pc->world;
+  x.rank = pc->rank;
+  x.mode = mode;
+  x.root = root;
+  x.slot = (int)(pc->seq & 1u);
+  x.off = pc->off_big;
+  x.max_elems = pc->max_elems;
+  x.n = n;
+  // every block of every rank adds one to each flag per exchange
+  x.target = (pc->seq / 2 + 1) * (unsigned)(pc->world * kPeerBlocks);
+  x.send = send;
+  x.recv = recv;
+  pc->seq += 1;
+  peer_exchange_kernel<<<kPeerBlocks, kPeerThreads, 0, s>>>(x);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 }  // namespace sr

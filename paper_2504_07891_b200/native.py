@@ -70,6 +70,14 @@ EXPORTS = {
     "sr_tp_comm_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     "sr_tp_comm_destroy": (C.c_int, [C.c_void_p]),
     "sr_model_set_tp": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sr_tp_peer_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int32,
+                                    C.POINTER(C.c_void_p)]),
+    "sr_tp_peer_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sr_tp_peer_open": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sr_tp_peer_base": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "sr_tp_peer_attach": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sr_tp_peer_destroy": (C.c_int, [C.c_void_p]),
+    "sr_model_set_tp_peer": (C.c_int, [C.c_void_p, C.c_void_p]),
 }
 
 _lib = None

@@ -16,8 +16,10 @@ from paper_2504_07891_b200.domain import BackendRole, render_generation_prompt
 from paper_2504_07891_b200.shapes import get_spec, make_weights
 from paper_2504_07891_b200.vocab import shared_vocab
 
+from tests.tolerance import floor_tol
+
 pytestmark = pytest.mark.gpu
-TOL = 5e-2
+TOL = floor_tol("tiny-base")  # tests/tolerance.py
 
 
 def _suffixes(v, n, lo, hi, seed):

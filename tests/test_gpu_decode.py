@@ -4,10 +4,11 @@
   (SR_DECODE=graph, the A/B reference) produce the same greedy tokens, except
   at flagged near-ties of the oracle;
 * full R1-1.5B shape: every decoded token is replay-checked against the CPU
-  fp32 oracle (teacher forcing).  Tolerance: a GPU token that is not the
-  oracle's argmax must be within `tol` of it, where tol = max(2e-2, 2 x the
-  max |GPU - oracle| logit error the prefill path shows on the same prompt)
-  -- the stated bf16-vs-fp32 bound of this shape.
+  fp32 oracle (teacher forcing): a GPU token that is not the oracle's argmax
+  must be within the stated tolerance of it (``tests/tolerance.py``: twice
+  the oracle's own fp32-vs-fp64 floor at this shape and depth);
+* long context (~6K, several pages per attention split): persistent kernel
+  and graph decode, each replayed on the oracle.
 """
 
 import os
@@ -19,6 +20,8 @@ from oracle.ref_engine import RefEngine
 from paper_2504_07891_b200.domain import BackendRole, render_generation_prompt
 from paper_2504_07891_b200.shapes import get_spec, make_weights
 from paper_2504_07891_b200.vocab import shared_vocab
+
+from tests.tolerance import floor_tol
 
 pytestmark = pytest.mark.gpu
 
@@ -66,10 +69,10 @@ def test_persistent_kernel_matches_graph_decode(cuda, name):
         if a != b:
             k = next(i for i, (x, y) in enumerate(zip(a, b)) if x != y)
             rows = _replay(ref, ids, a[: k + 1], v.n_text)
-            assert rows[-1][2] < 5e-2 or rows[-1][0] == rows[-1][1], (p, k, rows[-1])
+            assert rows[-1][2] < floor_tol(name) or rows[-1][0] == rows[-1][1], (p, k, rows[-1])
             flagged += 1
         for t, top, gap in _replay(ref, ids, a, v.n_text):
-            assert t == top or gap < 5e-2, (p, t, top, gap)
+            assert t == top or gap < floor_tol(name), (p, t, top, gap)
     print(f"{name}: persistent vs graph decode diverged (flagged near-ties) in {flagged}/4")
 
 
@@ -109,11 +112,11 @@ def test_full_size_draft_decode_replays_on_oracle(cuda):
     ref = RefEngine(spec, w, v)
     ids = v.encode(render_generation_prompt(v.problem(64, 3), ""))
     s = mk.pool.streams[0]
-    # prefill-path logit error on the prompt sets the stated tolerance
+    tol = floor_tol("r1-1.5b")
     got = mk.engine.forward_logits(s, ids).cpu()[:, : v.n_text]
     want = ref.logits_teacher_forced(ids)[:, : v.n_text]
     err = float((got - want).abs().max())
-    tol = max(2e-2, 2 * err)
+    assert err <= tol, (err, tol)
     mk.engine.truncate(s, 0)
     gen, _ = mk.engine.generate(s, ids, 24, ())
     margins = list(mk.engine.last_margins)
@@ -144,7 +147,7 @@ def test_persistent_kernel_long_context(cuda):
     ctx = torch.randint(16, v.n_text, (6000,), generator=g).tolist()
     a, _ = mk.engine.generate(mk.pool.streams[0], ctx, 24, ())
     b, _ = gr.engine.generate(gr.pool.streams[0], ctx, 24, ())
-    if a != b:
-        k = next(i for i, (x, y) in enumerate(zip(a, b)) if x != y)
-        lg = ref.logits_teacher_forced(ctx + a[:k])[-1][: v.n_text]
-        assert abs(float(lg[a[k]] - lg[b[k]])) < 5e-2, k
+    tol = floor_tol("tiny-base")
+    for gen in (a, b):  # each path against the oracle, not only against each other
+        for t, top, gap in _replay(ref, ctx, gen, v.n_text):
+            assert t == top or gap < tol, (t, top, gap)

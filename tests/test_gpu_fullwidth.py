@@ -7,8 +7,9 @@ GEMM tilings, attention groupings and LM-head sizes as the full models, with
 the identical seeded weights of those layers.  Checked against the CPU fp32
 oracle:
 
-* prefill logits of every position (tolerance: max-abs <= 5e-2, mean-abs <=
-  5e-3 -- the bf16-storage-vs-fp32 bound at this width, measured here);
+* prefill logits of every position (tolerance: max-abs <= max(2e-2, 2 x the
+  oracle's own fp32-vs-fp64 floor of this 2-layer slice, measured here on the
+  CPU), mean-abs <= max(2e-3, 3 x the mean floor);
 * greedy decode through the persistent kernel, replayed with teacher forcing
   (a token may differ from the oracle argmax only at a near-tie < tol);
 * the judge readout (score, accept) of verify prompts, except near-ties.
@@ -21,6 +22,7 @@ import pytest
 import torch
 
 from oracle.ref_engine import RefEngine, judge_readout
+from oracle.tree_oracle import readout_ambiguity
 from paper_2504_07891_b200.contract import VerificationRequest
 from paper_2504_07891_b200.domain import BackendRole, render_generation_prompt
 from paper_2504_07891_b200.shapes import get_spec, make_weights
@@ -28,8 +30,7 @@ from paper_2504_07891_b200.vocab import shared_vocab
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
-TOL_MAX, TOL_MEAN = 5e-2, 5e-3
-
+TOL_MAX, TOL_MEAN = 2e-2, 2e-3  # raised to the measured slice floors by the fixture
 
 @pytest.fixture(scope="module", params=["qwen2.5-7b", "qwq-32b"])
 def sliced(request, cuda):
@@ -41,6 +42,12 @@ def sliced(request, cuda):
     v = shared_vocab(spec.vocab_text)
     gpu = B200Backend(spec, BackendRole.BASE, weights=w, max_ctx=1024, record=True)
     ref = RefEngine(spec, w, v)
+    from tests.test_gpu_parity import noise_floor
+
+    ids = v.encode(render_generation_prompt(v.problem(64, 11), " ".join(v.words[500:600]) + " "))
+    fmax, fmean = noise_floor(spec, w, ids)
+    global TOL_MAX, TOL_MEAN
+    TOL_MAX, TOL_MEAN = max(2e-2, 2 * fmax), max(2e-3, 3 * fmean)
     return spec, gpu, ref, v
 
 
@@ -110,5 +117,6 @@ def test_judge_readout(sliced):
         if got == want.score:
             agree += 1
         else:
-            assert want.margin < TOL_MAX, (i, got, want)
+            amb = readout_ambiguity(ref.model.forward(ref.model.new_cache(), ids), v.n_text)
+            assert amb < TOL_MAX, (i, got, want, amb)
     assert agree >= 7

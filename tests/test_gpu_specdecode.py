@@ -1,8 +1,7 @@
 """Token-level speculation on the device (``sr_verify_tokens``): the base
 model's steps generated with a draft proposing tokens equal plain greedy
 device decoding, up to flagged near-ties (the verify pass uses the tensor-core
-prefill path, plain decode the persistent GEMV kernel; tolerance 5e-2 as the
-decode parity tests)."""
+prefill path, plain decode the persistent GEMV kernel; tolerance: tests/tolerance.py)."""
 
 import pytest
 
@@ -12,8 +11,10 @@ from paper_2504_07891_b200.domain import DEFAULT_STEP_STOP_MARKERS, BackendRole,
 from paper_2504_07891_b200.shapes import get_spec, make_weights
 from paper_2504_07891_b200.vocab import shared_vocab
 
+from tests.tolerance import floor_tol
+
 pytestmark = pytest.mark.gpu
-TOL = 5e-2
+TOL = floor_tol("tiny-base")  # tests/tolerance.py
 
 
 @pytest.mark.parametrize("draft_name", ["tiny-draft", "tiny-base"])
