@@ -16,7 +16,7 @@ from paper_2504_07891_b200.domain import BackendRole, render_generation_prompt
 from paper_2504_07891_b200.shapes import get_spec, make_weights
 from paper_2504_07891_b200.vocab import shared_vocab
 
-from tests.tolerance import floor_tol
+from tolerance import floor_tol
 
 pytestmark = pytest.mark.gpu
 TOL = floor_tol("tiny-base")  # tests/tolerance.py

@@ -11,7 +11,7 @@ from paper_2504_07891_b200.domain import DEFAULT_STEP_STOP_MARKERS, BackendRole,
 from paper_2504_07891_b200.shapes import get_spec, make_weights
 from paper_2504_07891_b200.vocab import shared_vocab
 
-from tests.tolerance import floor_tol
+from tolerance import floor_tol
 
 pytestmark = pytest.mark.gpu
 TOL = floor_tol("tiny-base")  # tests/tolerance.py
