@@ -877,7 +877,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
           }
           if (stop || s_stop) break;
           if (p.trace) p.trace[c * 8 + 3] = (int)n;
-          {
+          if (p.no_load) {  // experiment: consumer chain without the weight stream
+            const int nu = ld.hi - ld.u < kUPS ? ld.hi - ld.u : kUPS;
+            for (int q = 0; q < nu; ++q) ld.next(p, s_ph);
+            nld += nu;
+            mbar_arrive(&full[slot]);
+          } else {
             const int nu = ld.hi - ld.u < kUPS ? ld.hi - ld.u : kUPS;
             mbar_expect_tx(&full[slot], nu * ld.bytes);
             uint8_t* dst = ring + (size_t)slot * kStageBytes;

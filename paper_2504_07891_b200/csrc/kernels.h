@@ -239,6 +239,8 @@ struct MkParams {
   int bar_sleep;             // ns of backoff between grid-barrier polls
   int evict_first;           // stream weights with an L2 evict-first policy
   int min_pages;             // attention: minimum K/V pages per split
+  int no_load;               // SR_MK_NOLOAD experiment: stages handed out without loading
+                             // weights (times the consumer chain alone; results invalid)
   // tensor parallelism over NVLink peer memory (tp_world > 1): every rank's
   // exchange buffer (flags at the head, tp.cu), the decode / greedy mailboxes
   int tp_world, tp_rank, vocab_base, tp_dec_row;

@@ -295,6 +295,8 @@ struct Model {
     if (const char* v = getenv("SR_MK_MINPAGES")) p.min_pages = std::max(1, atoi(v));
     if (const char* v = getenv("SR_MK_EVICT_FIRST")) p.evict_first = atoi(v);
     if (const char* v = getenv("SR_MK_BARSLEEP")) p.bar_sleep = atoi(v);
+    p.no_load = 0;
+    if (const char* v = getenv("SR_MK_NOLOAD")) p.no_load = atoi(v);
     return 0;
   }
 

@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // Tensor parallelism of the base model.
 //
 // Megatron-style: each rank holds its q/k/v heads and gate/up units (column
@@ -421,6 +423,9 @@ int peer_exchange(PeerComm* pc, int mode, const float* send, float* recv, size_t
   x.send = send;
   x.recv = recv;
   pc->seq += 1;
+  static const bool log = getenv("SR_TP_LOG") != nullptr;
+  if (log) fprintf(stderr, "[peer] rank %d seq %u mode %d n %zu slot %d target %u\n", x.rank,
+                   pc->seq - 1, mode, n, x.slot, x.target);
   peer_exchange_kernel<<<kPeerBlocks, kPeerThreads, 0, s>>>(x);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

@@ -42,7 +42,7 @@ def sliced(request, cuda):
     v = shared_vocab(spec.vocab_text)
     gpu = B200Backend(spec, BackendRole.BASE, weights=w, max_ctx=1024, record=True)
     ref = RefEngine(spec, w, v)
-    from tests.test_gpu_parity import noise_floor
+    from test_gpu_parity import noise_floor
 
     ids = v.encode(render_generation_prompt(v.problem(64, 11), " ".join(v.words[500:600]) + " "))
     fmax, fmean = noise_floor(spec, w, ids)

@@ -282,3 +282,44 @@ def test_deterministic_and_rollback_idempotent(tiny):
         gpu.engine.truncate(s, 0)
     c = gpu.generate_step(req).text
     assert a == b == c
+
+
+def test_reference_engine_drives_gpu_backends_vs_golden(tiny, stepspec):
+    """The drop-in on the device: the *unmodified* reference engine
+    (``stepspec.engine.run_trajectory``, ``engine.py:297-354``) drives
+    ``build_pair("tiny", types=reference_types(stepspec))`` -- results bound to
+    the reference's own classes (``base.py:77-100``) -- and every C1 golden
+    trajectory (reference engine + oracle, ``tests/golden/make_golden.py``) is
+    reproduced up to a flagged near-tie, with ``validate_trajectory``
+    (``engine.py:715-754``) accepting each result."""
+    from stepspec import engine as reng
+    from stepspec.core import AcceptanceThreshold as RThr, EngineConfig as RCfg
+
+    from paper_2504_07891_b200.backend import build_pair
+    from paper_2504_07891_b200.host import reference_types
+
+    T = reference_types(stepspec)
+    small, base = build_pair("tiny", max_ctx=2048, types=T, record=True)
+    v = shared_vocab(4096)
+    verdicts = []
+    for case in (c for c in GOLDEN["cases"] if c["kind"] == "spec_reason"):
+        small.calls.clear()
+        base.calls.clear()
+        base.threshold = case["threshold"]
+        cfg = RCfg(threshold=RThr(case["threshold"]), **C1)
+        res = reng.run_trajectory(cfg, v.problem(64, case["problem_seed"]), small, base)
+        reng.validate_trajectory(res, cfg)
+        scores = [s.score for s in list(res.state.retained_steps) + list(res.rejected_steps)
+                  if s.score is not None]
+        assert all(type(x) is T.UtilityScore for x in scores)
+        if json.loads(json.dumps(trace_signature(res))) == case["signature"]:
+            verdicts.append("identical")
+            continue
+        vs = _first_divergence(small.calls, case["small_calls"], tiny["tiny-draft"][1], v,
+                               tiny["tiny-draft"][2]["max"])
+        vb = _first_divergence(base.calls, case["base_calls"], tiny["tiny-base"][1], v,
+                               tiny["tiny-base"][2]["max"])
+        assert "flagged" in (vs[0], vb[0]), (case["problem_seed"], case["threshold"], vs, vb)
+        verdicts.append("flagged")
+    print("reference-engine golden verdicts", verdicts)
+    assert verdicts
