@@ -61,9 +61,7 @@ namespace sr {
 constexpr int kMkWarps = SR_MK_WARPS;      // consumer warps (16 or 8)
 constexpr int kMkConsumers = kMkWarps * 32;
 constexpr int kRW = 32 / kMkWarps;          // rows of a 32-row tile per warp
-constexpr int kGroups = kMkConsumers / 128; // attention P.V position groups
-constexpr int kPPG = 64 / kGroups;          // positions per P.V group
-constexpr int kPosPass = 4 * kMkWarps;      // positions per score pass
+static_assert(kMkWarps == 16, "attention: warp w owns head dims 8w..8w+7 of P.V");
 constexpr int kMkThreads = kMkConsumers + 32;
 constexpr int kTR = 32;                    // tile rows
 constexpr int kTC = 256;                   // tile columns (bf16)
@@ -79,10 +77,9 @@ constexpr int kStageBytes = kUPS * kTileBytes;
 constexpr int kMkMaxStages = 13;
 constexpr int kMkMaxGq = 8;
 constexpr int kMkProfEvents = SR_PROF_EVENTS;
-constexpr int kMkAttnScratchFloats =
-    kMkMaxGq * 128 + kMkMaxGq * 64 + 3 * kMkMaxGq + kGroups * kMkMaxGq * 128 + 2 * 128;
-constexpr int kMkTab = 256;
-constexpr int kKvBufBytes = 2 * kPage * kHeadDim * 2;  // 32 KB  // max 32-row blocks of a tile-range phase (smem tables)
+constexpr int kMkAttnScratchFloats = 1536;  // attention q / P / row partials; COMBINE [16][32]+32
+constexpr int kMkTab = 256;  // max 32-row blocks of a tile-range phase (smem tables)
+constexpr int kKvBufBytes = 2 * kPage * kHeadDim * 2;  // K + V page (32 KB)
 
 enum { PH_QKV = 0, PH_O = 1, PH_GU = 2, PH_D = 3, PH_LM = 4 };
 
@@ -460,20 +457,66 @@ SR_DEV float mk_qkv_val(const MkParams& p, const __nv_bfloat16* bias, const uint
   return mk_sum_parts(p.part_qkv, tab, row, p.maxj) + bf_to_f(bias[row]);
 }
 
-// one K page + one V page (16 KB each, contiguous in the pools) -> shared
-// memory with two 1-D bulk copies on one mbarrier (issued by thread 0)
-SR_DEV void mk_fetch_page(const MkParams& p, int layer, int g, int page, uint8_t* kvbuf,
-                          uint64_t* kvbar) {
-  const size_t off = kv_offset(layer, page, g, 0, p.n_pages, p.KV);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_expect_tx(kvbar, 2 * kPage * kHeadDim * 2);
-  bulk_load_1d(kvbuf, p.k_pool + off, kPage * kHeadDim * 2, kvbar);
-  bulk_load_1d(kvbuf + kPage * kHeadDim * 2, p.v_pool + off, kPage * kHeadDim * 2, kvbar);
+// K and V pages land in shared memory as two 64-position x 64-dim boxes each
+// (dims 0-63, 64-127; 8 KB), 128-B swizzled by TMA: 16-B chunk c of position
+// r sits at r * 128 + ((c ^ (r & 7)) << 4), so the 8 rows of every 8x8
+// ldmatrix block fall on distinct banks.  Two TMA ops per page (the pools'
+// tensor maps follow the weight maps in p.maps).
+constexpr int kQRow = kHeadDim + 8;                  // staged q rows (8 heads), padded
+constexpr int kPRow = kPage + 8;                     // staged P rows (bf16), padded
+constexpr int kKvTile = kPage * 64 * 2;              // one 64 x 64 box
+
+SR_DEV uint32_t kv_swz(int r, int chunk) {  // byte offset of (position r, 16-B chunk 0..15)
+  return (chunk >> 3) * kKvTile + r * 128 + (((chunk & 7) ^ (r & 7)) << 4);
 }
 
-// Attention of kv head g over pages [p0, p1) for its Gq query heads; the split
-// partials (m, l, O) go to apart, and the last split CTA of g to finish (atomic
-// ticket) merges all splits of g into the bf16 attention output.
+// thread 0: one page of the K (which = 0) or V (1) pool (kv head g of `layer`) -> dst
+SR_DEV void mk_fetch_tile(const MkParams& p, int which, int layer, int g, int page, uint8_t* dst,
+                          uint64_t* bar) {
+  const CUtensorMap* map = p.maps + p.L * 4 + 1 + which;
+  const int row = (int)((((size_t)layer * p.n_pages + page) * p.KV + g) * kPage);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(bar, 2 * kKvTile);
+  tma_load_2d(dst, map, bar, 0, row);
+  tma_load_2d(dst + kKvTile, map, bar, 64, row);
+}
+
+SR_DEV void ldsm_x2(uint32_t& r0, uint32_t& r1, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(addr));
+}
+SR_DEV void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+SR_DEV void ldsm_x4t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+// m16n8k16 bf16 MMA, fp32 accumulate; rows 8-15 of A are zero (<= 8 heads)
+SR_DEV void mma16816(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+// Attention of kv head g over pages [p0, p1) for its query heads [jl, jh)
+// (<= 8: the MMA's rows 0-7, rows 8-15 zero), on the tensor cores:
+//   S = Q.K^T  warps 0-7, warp w = positions 8w..8w+7 of the page (m16n8k16,
+//              Q and K by ldmatrix from the padded smem rows)
+//   softmax    online, exp2, fp32; P kept as bf16 hi + lo (~16 mantissa bits,
+//              the oracle's P is fp32)
+//   O += P.V   all 16 warps, warp w = dims 8w..8w+7 (V by ldmatrix.trans)
+// K and V have their own mbarriers, so the next page's K is in flight while
+// this page's softmax and P.V run.  The new position's k / v (summed from the
+// qkv partials here) are written into the staged page rows before use, and V
+// rows past the context are zeroed (P is 0 there, but 0 * NaN is not).
+// Split partials (m, l, O) go to apart; COMBINE merges them.
 SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_table,
                          const __nv_bfloat16* bias, const uint16_t* tab, int c, int S_a,
                          int hs, int npages, float* sm, uint8_t* kvbuf, uint64_t* kvbar, uint32_t& kvpar) {
@@ -481,41 +524,59 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
   const int g = c / S_a, s = (c % S_a) / hs, hp = (c % S_a) % hs, PS = S_a / hs;
   if (g >= p.KV) return;  // uniform per CTA
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gr = lane >> 2, tq = lane & 3;  // MMA fragment row / column pair
   const int p0 = (int)((long long)npages * s / PS), p1 = (int)((long long)npages * (s + 1) / PS);
-  // query heads [jl, jh) of the group are this CTA's; the other heads' partial
-  // slots stay (m, l, O) = (-inf, 0, 0), which the combine skips
-  const int jl = Gq * hp / hs, jh = Gq * (hp + 1) / hs;
-  float* qs = sm;                              // [8][128]
-  float* ps = qs + kMkMaxGq * 128;             // [8][64]
-  float* alph = ps + kMkMaxGq * 64;            // [8]
-  float* mrun = alph + kMkMaxGq;               // [8]
-  float* lrun = mrun + kMkMaxGq;               // [8]
-  float* red = lrun + kMkMaxGq;                // [4][8][128]
-  float* kn = red + kGroups * kMkMaxGq * 128;  // [128] new k (rotated, bf16 values)
-  float* vn = kn + 128;                        // [128] new v
+  const int jl = Gq * hp / hs, jh = Gq * (hp + 1) / hs, nh = jh - jl;
+  __nv_bfloat16* qb = reinterpret_cast<__nv_bfloat16*>(sm);          // [8][kQRow]
+  __nv_bfloat16* pbh = qb + 8 * kQRow;                               // [8][kPRow] P hi
+  __nv_bfloat16* pbl = pbh + 8 * kPRow;                              // [8][kPRow] P lo
+  float* red_max = reinterpret_cast<float*>(pbl + 8 * kPRow);        // [8 warps][8 rows]
+  float* red_sum = red_max + 64;                                     // [8 warps][8 rows]
+  __nv_bfloat16* knb = reinterpret_cast<__nv_bfloat16*>(red_sum + 64);  // [128] new k
+  __nv_bfloat16* vnb = knb + kHeadDim;                                  // [128] new v
+  // page buffer b: K at kvb[b], V at kvb[b] + 2 boxes; mbarriers kvbar[2b] (K),
+  // kvbar[2b + 1] (V), phase parity in bit j of kvpar for barrier j.  With
+  // kv_dbl pages alternate between the two buffers and page k + 2 is fetched
+  // as soon as page k is done; else K / V of page k + 1 go out as soon as this
+  // page's S / P.V no longer need the single buffer.
+  const bool dbl = p.kv_dbl != 0;
+  uint8_t* const kvb[2] = {kvbuf, kvbuf + kKvBufBytes};
+  const int np = p1 - p0;
+  auto fetch = [&](int k, int which) {  // thread 0: K (0) or V (1) of local page k
+    const int b = dbl ? (k & 1) : 0;
+    mk_fetch_tile(p, which, layer, g, page_table[p0 + k], kvb[b] + which * 2 * kKvTile,
+                  kvbar + 2 * b + which);
+  };
   const float scale = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
-  const int sub = lane & 7;
-  const int dd = tid % kHeadDim, grp = tid / kHeadDim;
 
   const bool sub_prof = p.prof && c == 0 && tid == 0 && layer == 1;
   int sev = 0;
 #define SUB_EV() \
   do { if (sub_prof && sev < 32) p.prof[1600 + sev++] = global_ns(); } while (0)
   SUB_EV();
-  // first page's K/V copy goes out before anything else (independent of q)
-  if (tid == 0) mk_fetch_page(p, layer, g, page_table[p0], kvbuf, kvbar);
-  const __nv_bfloat16* ks = reinterpret_cast<const __nv_bfloat16*>(kvbuf);
-  const __nv_bfloat16* vs = ks + kPage * kHeadDim;
-  for (int t = tid; t < (jh - jl) * kHalf; t += kMkConsumers) {
-    const int j = jl + t / kHalf, i = t % kHalf;
-    const int r0 = (g * Gq + j) * kHeadDim + i;
-    const float v0 = mk_qkv_val(p, bias, tab, r0), v1 = mk_qkv_val(p, bias, tab, r0 + kHalf);
-    const float cs = p.rope[((size_t)pos * kHalf + i) * 2], sn = p.rope[((size_t)pos * kHalf + i) * 2 + 1];
-    // layout [head][e4][sub][4]: dim = sub*16 + e4*4 + k, so the 8 lanes of a
-    // position group read 8 consecutive float4 (conflict-free)
-    const int i2 = i + kHalf;
-    qs[j * 128 + ((i & 15) >> 2) * 32 + (i >> 4) * 4 + (i & 3)] = round_bf16(v0 * cs - v1 * sn);
-    qs[j * 128 + ((i2 & 15) >> 2) * 32 + (i2 >> 4) * 4 + (i2 & 3)] = round_bf16(v1 * cs + v0 * sn);
+  // first page's K / V copies go out before anything else (independent of q)
+  if (tid == 0) {
+    fetch(0, 0);
+    fetch(0, 1);
+    if (dbl && np > 1) {
+      fetch(1, 0);
+      fetch(1, 1);
+    }
+  }
+  // q of this CTA's heads: qkv partials + bias, RoPE, bf16 (the oracle's
+  // storage point); rows nh..7 zero
+  for (int t = tid; t < 8 * kHalf; t += kMkConsumers) {
+    const int r = t / kHalf, i = t % kHalf;
+    float y0 = 0.f, y1 = 0.f;
+    if (r < nh) {
+      const int r0 = (g * Gq + jl + r) * kHeadDim + i;
+      const float v0 = mk_qkv_val(p, bias, tab, r0), v1 = mk_qkv_val(p, bias, tab, r0 + kHalf);
+      const float cs = p.rope[((size_t)pos * kHalf + i) * 2], sn = p.rope[((size_t)pos * kHalf + i) * 2 + 1];
+      y0 = v0 * cs - v1 * sn;
+      y1 = v1 * cs + v0 * sn;
+    }
+    qb[r * kQRow + i] = __float2bfloat16_rn(y0);
+    qb[r * kQRow + i + kHalf] = __float2bfloat16_rn(y1);
   }
   const bool has_new = p1 == npages;
   if (has_new) {  // new position: k / v from the partials; appended to the pool
@@ -532,151 +593,138 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
         p.k_pool[base + tid] = y0;
         p.k_pool[base + tid + kHalf] = y1;
       }
-      kn[tid] = bf_to_f(y0);
-      kn[tid + kHalf] = bf_to_f(y1);
+      knb[tid] = y0;
+      knb[tid + kHalf] = y1;
     } else if (tid < kHalf + kHeadDim) {
       const int d2 = tid - kHalf;
       const int r = p.q_dim + p.kv_dim + g * kHeadDim + d2;
       const __nv_bfloat16 y = __float2bfloat16_rn(mk_qkv_val(p, bias, tab, r));
       if (hp == 0) p.v_pool[base + d2] = y;
-      vn[d2] = bf_to_f(y);
+      vnb[d2] = y;
     }
   }
-  if (tid < kMkMaxGq) {
-    mrun[tid] = -INFINITY;
-    lrun[tid] = 0.f;
-  }
-  float acc[kMkMaxGq];
-#pragma unroll
-  for (int j = 0; j < kMkMaxGq; ++j) acc[j] = 0.f;
+  float o[4] = {0.f, 0.f, 0.f, 0.f};  // O rows gr (c0, c1) of dims 8*warp + 2*tq, +1
+  float m_run = -INFINITY, l_run = 0.f;  // row gr, identical in every thread of the row
   cbar();
   SUB_EV();  // q / new k,v ready
+  const uint32_t q_addr = smem_u32(qb) + (lane & 7) * kQRow * 2 + (lane >> 3) * 16;
+  // K: position 8w + (lane & 7), chunk 2kk + (lane >> 3); V: position
+  // (lane >> 3) * 8 + (lane & 7) (+16ks), chunk w (dims 8w..8w+7)
+  const int kr = 8 * (warp & 7) + (lane & 7), vr = (lane >> 3) * 8 + (lane & 7);
+  const uint32_t p_addr = smem_u32(pbh) + (lane & 7) * kPRow * 2 + (lane >> 3) * 16;
 
-  for (int pg_i = p0; pg_i < p1; ++pg_i) {
+  for (int k = 0; k < np; ++k) {
+    const int pg_i = p0 + k;
     const int P0 = pg_i * kPage;
     const int nval = min(kPage, pos + 1 - P0);
-    const int newl = has_new && pg_i == p1 - 1 ? pos - P0 : -1;  // slot of the new position
-    mbar_wait(kvbar, kvpar);
-    kvpar ^= 1u;
+    const bool last = has_new && pg_i == p1 - 1;  // holds the new position at nval - 1
+    const int b = dbl ? (k & 1) : 0;
+    uint8_t* kbuf = kvb[b];
+    uint8_t* vbuf = kbuf + 2 * kKvTile;
+    const uint32_t k_smem = smem_u32(kbuf), v_smem = smem_u32(vbuf);
+    mbar_wait(kvbar + 2 * b, (kvpar >> (2 * b)) & 1u);
+    kvpar ^= 1u << (2 * b);
+    if (last) {
+      if (tid < kHeadDim / 8)
+        *reinterpret_cast<uint4*>(kbuf + kv_swz(nval - 1, tid)) = reinterpret_cast<const uint4*>(knb)[tid];
+      cbar();
+    }
     SUB_EV();  // page landed
-    // scores: 8 lanes per position, 16 dims per lane
+    if (warp < 8) {  // S for positions 8w..8w+7, rows gr: c0, c1 = positions 8w + 2tq, +1
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int pass = 0; pass < 64 / kPosPass; ++pass) {
-      const int posl = pass * kPosPass + warp * 4 + (lane >> 3);
-      float sc[kMkMaxGq];
-#pragma unroll
-      for (int j = 0; j < kMkMaxGq; ++j) sc[j] = 0.f;
-      if (posl < nval) {
-        float kf[16];
-        if (posl == newl) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) kf[e] = kn[sub * 16 + e];
-        } else {
-          const uint4* kr = reinterpret_cast<const uint4*>(ks + posl * kHeadDim + sub * 16);
-          const uint4 k0 = kr[0], k1 = kr[1];
-          const uint32_t kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float2 f2 = bf2_to_f2(kw[e]);
-            kf[2 * e] = f2.x;
-            kf[2 * e + 1] = f2.y;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kMkMaxGq; ++j) {
-          if (j >= jl && j < jh) {
-            float a = 0.f;
-#pragma unroll
-            for (int e4 = 0; e4 < 4; ++e4) {
-              const float4 q4 = *reinterpret_cast<const float4*>(qs + j * 128 + e4 * 32 + sub * 4);
-              a = fmaf(q4.x, kf[4 * e4], a);
-              a = fmaf(q4.y, kf[4 * e4 + 1], a);
-              a = fmaf(q4.z, kf[4 * e4 + 2], a);
-              a = fmaf(q4.w, kf[4 * e4 + 3], a);
-            }
-            sc[j] = a;
-          }
-        }
+      for (int kk = 0; kk < kHeadDim / 16; kk += 2) {
+        uint32_t a[4], b[4];
+        ldsm_x4(a, q_addr + kk * 32);   // rows 0-7: dims 16kk..+7, +8..15, 16(kk+1).., +8..
+        ldsm_x4(b, k_smem + kv_swz(kr, 2 * kk + (lane >> 3)));  // positions 8w..+7: same dims
+        mma16816(sc, a[0], a[1], b[0], b[1]);
+        mma16816(sc, a[2], a[3], b[2], b[3]);
       }
+      const int c0p = 8 * warp + 2 * tq;
+      const float s0 = c0p < nval ? sc[0] * scale : -INFINITY;
+      const float s1 = c0p + 1 < nval ? sc[1] * scale : -INFINITY;
+      float mx = fmaxf(s0, s1);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      if (tq == 0) red_max[warp * 8 + gr] = mx;
+      sc[0] = s0;
+      sc[1] = s1;
+      cbar();  // (1) page max partials in; K buffer free
+      if (tid == 0 && !dbl && k + 1 < np) fetch(k + 1, 0);
+      float pm = red_max[gr];
 #pragma unroll
-      for (int j = 0; j < kMkMaxGq; ++j) {
-        if (j >= jl && j < jh) {
-          float a = sc[j];
-          a += __shfl_xor_sync(0xffffffffu, a, 1);
-          a += __shfl_xor_sync(0xffffffffu, a, 2);
-          a += __shfl_xor_sync(0xffffffffu, a, 4);
-          if (sub == 0) ps[j * 64 + posl] = posl < nval ? a * scale : -INFINITY;
-        }
-      }
-    }
-    cbar();
-    SUB_EV();  // scores
-    if (warp >= jl && warp < jh) {  // online softmax of head `warp` over this page
-      const int j = warp;
-      const float s0 = ps[j * 64 + lane], s1 = ps[j * 64 + lane + 32];
-      const float mx = warp_max(fmaxf(s0, s1));
-      const float m_old = mrun[j];
-      const float m_new = fmaxf(m_old, mx);
+      for (int w2 = 1; w2 < 8; ++w2) pm = fmaxf(pm, red_max[w2 * 8 + gr]);
+      const float m_new = fmaxf(m_run, pm);
       const float e0 = exp2f(s0 - m_new), e1 = exp2f(s1 - m_new);
-      const float sum = warp_sum(e0 + e1);
-      ps[j * 64 + lane] = e0;
-      ps[j * 64 + lane + 32] = e1;
-      __syncwarp();
-      if (lane == 0) {
-        const float a = exp2f(m_old - m_new);
-        alph[j] = a;
-        lrun[j] = lrun[j] * a + sum;
-        mrun[j] = m_new;
+      const __nv_bfloat16 h0 = __float2bfloat16_rn(e0), h1 = __float2bfloat16_rn(e1);
+      __nv_bfloat162 hi, lo;
+      hi.x = h0;
+      hi.y = h1;
+      lo.x = __float2bfloat16_rn(e0 - __bfloat162float(h0));
+      lo.y = __float2bfloat16_rn(e1 - __bfloat162float(h1));
+      *reinterpret_cast<__nv_bfloat162*>(pbh + gr * kPRow + c0p) = hi;
+      *reinterpret_cast<__nv_bfloat162*>(pbl + gr * kPRow + c0p) = lo;
+      float rs = e0 + e1;
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+      if (tq == 0) red_sum[warp * 8 + gr] = rs;
+    } else {
+      cbar();  // (1)
+    }
+    // every thread: the rows' new max and the rescale of its O / l
+    float pm = red_max[gr];
+#pragma unroll
+    for (int w2 = 1; w2 < 8; ++w2) pm = fmaxf(pm, red_max[w2 * 8 + gr]);
+    const float m_new = fmaxf(m_run, pm);
+    const float alpha = exp2f(m_run - m_new);
+    m_run = m_new;
+    o[0] *= alpha;
+    o[1] *= alpha;
+    mbar_wait(kvbar + 2 * b + 1, (kvpar >> (2 * b + 1)) & 1u);
+    kvpar ^= 1u << (2 * b + 1);
+    if (last) {  // new v row; rows past the context zeroed
+      for (int t = tid; t < (kPage - nval + 1) * 16; t += kMkConsumers) {
+        const int r = nval - 1 + t / 16, q = t % 16;
+        *reinterpret_cast<uint4*>(vbuf + kv_swz(r, q)) =
+            r == nval - 1 ? reinterpret_cast<const uint4*>(vnb)[q] : make_uint4(0, 0, 0, 0);
       }
     }
-    cbar();
+    cbar();  // (2) P, row sums and the staged V in
     {
-      float vf[kPPG];
+      float rs = red_sum[gr];
 #pragma unroll
-      for (int q = 0; q < kPPG; ++q) vf[q] = bf_to_f(vs[(grp * kPPG + q) * kHeadDim + dd]);
-      if (newl >= grp * kPPG && newl < grp * kPPG + kPPG) {
+      for (int w2 = 1; w2 < 8; ++w2) rs += red_sum[w2 * 8 + gr];
+      l_run = l_run * alpha + rs;
+    }
 #pragma unroll
-        for (int q = 0; q < kPPG; ++q)
-          if (grp * kPPG + q == newl) vf[q] = vn[dd];
-      }
-#pragma unroll
-      for (int j = 0; j < kMkMaxGq; ++j)
-        if (j >= jl && j < jh) acc[j] *= alph[j];
-#pragma unroll
-      for (int q = 0; q < kPPG; ++q)
-        if (grp * kPPG + q >= nval) vf[q] = 0.f;  // slots past the context may hold garbage
-#pragma unroll
-      for (int j = 0; j < kMkMaxGq; ++j) {
-        if (j >= jl && j < jh) {
-#pragma unroll
-          for (int q4 = 0; q4 < kPPG / 4; ++q4) {
-            const float4 pp = *reinterpret_cast<const float4*>(ps + j * 64 + grp * kPPG + q4 * 4);
-            acc[j] = fmaf(pp.x, vf[4 * q4], acc[j]);
-            acc[j] = fmaf(pp.y, vf[4 * q4 + 1], acc[j]);
-            acc[j] = fmaf(pp.z, vf[4 * q4 + 2], acc[j]);
-            acc[j] = fmaf(pp.w, vf[4 * q4 + 3], acc[j]);
-          }
-        }
+    for (int ks = 0; ks < kPage / 16; ks += 2) {
+      uint32_t ah[4], al[4], b[4];
+      ldsm_x4(ah, p_addr + ks * 32);
+      ldsm_x4(al, p_addr + 8 * kPRow * 2 + ks * 32);
+      ldsm_x4t(b, v_smem + kv_swz(vr + 16 * ks, warp));  // positions 16ks..16ks+31, dims 8w..+7
+      mma16816(o, ah[0], ah[1], b[0], b[1]);
+      mma16816(o, al[0], al[1], b[0], b[1]);
+      mma16816(o, ah[2], ah[3], b[2], b[3]);
+      mma16816(o, al[2], al[3], b[2], b[3]);
+    }
+    cbar();  // (3) V, P and the row partials free
+    if (tid == 0) {
+      if (!dbl && k + 1 < np) fetch(k + 1, 1);
+      if (dbl && k + 2 < np) {
+        fetch(k + 2, 0);
+        fetch(k + 2, 1);
       }
     }
-    cbar();  // page buffer free
-    if (pg_i + 1 < p1 && tid == 0) mk_fetch_page(p, layer, g, page_table[pg_i + 1], kvbuf, kvbar);
+    SUB_EV();
   }
-#pragma unroll
-  for (int j = 0; j < kMkMaxGq; ++j)
-    if (j < Gq) red[(grp * kMkMaxGq + j) * 128 + dd] = acc[j];
-  cbar();
-  if (grp == 0) {
-    for (int j = 0; j < Gq; ++j) {
-      float o = 0.f;
-#pragma unroll
-      for (int g2 = 0; g2 < kGroups; ++g2) o += red[(g2 * kMkMaxGq + j) * 128 + dd];
-      p.apart[((size_t)c * kMkMaxGq + j) * 130 + dd] = o;
+  // partials: O rows gr < nh (head jl + gr), dims 8w + 2tq, +1; m / l
+  if (gr < nh) {
+    float* a = p.apart + ((size_t)c * kMkMaxGq + jl + gr) * 130;
+    *reinterpret_cast<float2*>(a + 8 * warp + 2 * tq) = make_float2(o[0], o[1]);
+    if (warp == 0 && tq == 0) {
+      a[128] = m_run;
+      a[129] = l_run;
     }
-  }
-  if (tid < Gq) {
-    p.apart[((size_t)c * kMkMaxGq + tid) * 130 + 128] = mrun[tid];
-    p.apart[((size_t)c * kMkMaxGq + tid) * 130 + 129] = lrun[tid];
   }
   SUB_EV();  // partial written
 #undef SUB_EV
@@ -814,7 +862,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   __shared__ int s_tok;
   __shared__ uint16_t s_tab[3][kMkTab];  // contributor tables: qkv, o, down
   __shared__ PhaseInfo s_ph[5];
-  __shared__ __align__(8) uint64_t kvbar;
+  __shared__ __align__(8) uint64_t kvbar[4];  // K, V of page buffer 0; K, V of buffer 1
   __shared__ float s_margin, s_rv1, s_rv2;
   __shared__ volatile int s_stop;
 
@@ -825,7 +873,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   uint8_t* kvbuf = mk_smem + (size_t)S * kStageBytes;  // one K page + one V page
   float* kvtmp = reinterpret_cast<float*>(kvbuf);         // prologue scratch (d <= 5120)
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(kvbuf + kKvBufBytes);
-  float* scratch = reinterpret_cast<float*>(xs);
+  // attention: second page buffer at xs (1024-aligned), scratch behind it
+  float* scratch = reinterpret_cast<float*>(kvbuf + kKvBufBytes + (p.kv_dbl ? kKvBufBytes : 0));
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -833,7 +882,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       mbar_init(&empty[i], kMkWarps);
     }
     s_stop = 0;
-    mbar_init(&kvbar, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&kvbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < 5) s_ph[threadIdx.x] = mk_phase_info(p, threadIdx.x, blockIdx.x, gridDim.x);
@@ -977,7 +1026,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       // attention (+ merge of the splits by the last split CTA of each kv head)
       const uint64_t ta0 = global_ns();
       mk_attention(p, l, pos, page_table, ly.bqkv, s_tab[0], c, S_a, hs, npages, scratch, kvbuf,
-                   &kvbar, kvpar);
+                   kvbar, kvpar);
       if (p.prof && threadIdx.x == 0 && l == 1 && tstep < 40) {  // per-CTA attention time, layer 1
         p.prof[1280 + c] = global_ns() - ta0;
         p.prof[1440 + c] = (c % S_a) == S_a - 1;
@@ -1108,17 +1157,25 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
 }
 
 // ------------------------------------------------------------------- host ---
-size_t mk_smem_bytes(int stages, int xs_elems) {
+// ring | K/V page buffer | vector region: the GEMV input x, which during
+// attention holds the attention scratch and, with kv_dbl, a second K/V page
+// buffer in front of it
+size_t mk_smem_bytes(int stages, int xs_elems, int kv_dbl) {
   size_t xs = (size_t)xs_elems * 2;
-  const size_t attn = (size_t)kMkAttnScratchFloats * 4;
+  const size_t attn = (size_t)kMkAttnScratchFloats * 4 + (kv_dbl ? kKvBufBytes : 0);
   if (xs < attn) xs = attn;
   return (size_t)stages * kStageBytes + kKvBufBytes + xs;
 }
 
 int mk_pick_stages(int xs_elems) {
   int s = kMkMaxStages;
-  while (s > 2 && mk_smem_bytes(s, xs_elems) > 225 * 1024) --s;
+  while (s > 2 && mk_smem_bytes(s, xs_elems, 0) > 225 * 1024) --s;
   return s;
+}
+
+// double-buffer the attention pages when that costs no ring stage
+int mk_pick_kv_dbl(int stages, int xs_elems) {
+  return mk_smem_bytes(stages, xs_elems, 1) <= 225 * 1024 ? 1 : 0;
 }
 
 int mk_max_j(int N, int K, int num_sms) {
@@ -1132,7 +1189,7 @@ int mk_tile_rows() { return kTR; }
 int mk_tile_cols() { return kTC; }
 
 cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream) {
-  const size_t smem = mk_smem_bytes(p.stages, p.xs_elems);
+  const size_t smem = mk_smem_bytes(p.stages, p.xs_elems, p.kv_dbl);
   static size_t attr = 0;
   if (attr < smem) {
     cudaError_t e =

@@ -239,6 +239,7 @@ struct MkParams {
   int bar_sleep;             // ns of backoff between grid-barrier polls
   int evict_first;           // stream weights with an L2 evict-first policy
   int min_pages;             // attention: minimum K/V pages per split
+  int kv_dbl;                // attention pages double-buffered (second buffer in the x region)
   int no_load;               // SR_MK_NOLOAD experiment: stages handed out without loading
                              // weights (times the consumer chain alone; results invalid)
   // tensor parallelism over NVLink peer memory (tp_world > 1): every rank's
@@ -248,8 +249,9 @@ struct MkParams {
   size_t tp_off_dec, tp_off_lm;
 };
 
-size_t mk_smem_bytes(int stages, int xs_elems);
+size_t mk_smem_bytes(int stages, int xs_elems, int kv_dbl);
 int mk_pick_stages(int xs_elems);
+int mk_pick_kv_dbl(int stages, int xs_elems);
 int mk_max_j(int N, int K, int num_sms);
 int mk_tile_rows();
 int mk_tile_cols();

@@ -100,7 +100,7 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
   const int qd_i = d.n_heads * SR_HEAD_DIM, qkv_i = qd_i + 2 * d.n_kv_heads * SR_HEAD_DIM;
   L.mk_maxj = std::max({mk_max_j(qkv_i, d.d_model, mk_g), mk_max_j(d.d_model, qd_i, mk_g),
                         mk_max_j(d.d_model, d.d_ffn, mk_g)});
-  L.mk_maps = take(((size_t)d.n_layers * 4 + 1) * sizeof(CUtensorMap));
+  L.mk_maps = take(((size_t)d.n_layers * 4 + 3) * sizeof(CUtensorMap));  // + K, V pools
   L.mk_layers = take((size_t)d.n_layers * sizeof(MkLayer));
   L.mk_h = take(2 * (size_t)d.d_model * 4);
   L.mk_part = take(3 * (size_t)mk_g * L.mk_maxj * mk_tile_rows() * 4);
@@ -192,7 +192,9 @@ struct Model {
   // persistent decode kernel, written into the workspace once
   int build_mk() {
     const int n = d.n_layers * 4 + 1;
-    std::vector<TMap> maps(n);
+    std::vector<TMap> maps(n + 2);
+    maps[n] = kvmaps[0];  // K / V pools, 64 x 64 boxes, 128-B swizzle (decode attention)
+    maps[n + 1] = kvmaps[1];
     for (int l = 0; l < d.n_layers; ++l) {
       const void* w[4] = {lw(l, WQKV), lw(l, WO), lw(l, WGU), lw(l, WD)};
       const int rows[4] = {qkv_rows, d.d_model, 2 * d.d_ffn, d.d_model};
@@ -234,7 +236,7 @@ struct Model {
     }
     std::vector<MkLayer> ly(d.n_layers);
     for (int l = 0; l < d.n_layers; ++l) ly[l] = MkLayer{lw(l, LN1), lw(l, BQKV), lw(l, LN2), nullptr};
-    SR_CK(cudaMemcpy(ws + L.mk_maps, maps.data(), n * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    SR_CK(cudaMemcpy(ws + L.mk_maps, maps.data(), (n + 2) * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     SR_CK(cudaMemcpy(ws + L.mk_layers, ly.data(), ly.size() * sizeof(MkLayer),
                      cudaMemcpyHostToDevice));
     MkParams& p = mk;
@@ -283,6 +285,8 @@ struct Model {
     const int tc = mk_tile_cols();
     p.xs_elems = (std::max({d.d_model, q_dim, d.d_ffn}) + tc - 1) / tc * tc;
     p.stages = mk_pick_stages(p.xs_elems);
+    p.kv_dbl = mk_pick_kv_dbl(p.stages, p.xs_elems);
+    if (const char* v = getenv("SR_MK_KVDBL")) p.kv_dbl = p.kv_dbl && atoi(v) != 0;
     // L2 prefetch run-ahead beyond the ring (tiles); off by default: measured
     // slower on B200 (the extra HBM traffic delays the latency-bound phases)
     p.l2_ahead = -1;
