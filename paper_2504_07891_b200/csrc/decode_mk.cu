@@ -77,7 +77,7 @@ constexpr int kStageBytes = kUPS * kTileBytes;
 constexpr int kMkMaxStages = 13;
 constexpr int kMkMaxGq = 8;
 constexpr int kMkProfEvents = SR_PROF_EVENTS;
-constexpr int kMkAttnScratchFloats = 1536;  // attention q / P / row partials; COMBINE [16][32]+32
+constexpr int kMkAttnScratchFloats = 2048;  // attention q / P / row partials; COMBINE [16][32]+32
 constexpr int kMkTab = 256;  // max 32-row blocks of a tile-range phase (smem tables)
 constexpr int kKvBufBytes = 2 * kPage * kHeadDim * 2;  // K + V page (32 KB)
 
@@ -214,13 +214,62 @@ SR_DEV void mk_grid_sync(unsigned* ctr, unsigned& target, int G, int sleep_ns) {
 SR_DEV void mk_norm_prologue(const MkParams& p, int mode, int tok, const float* hin,
                              const float* part, const uint16_t* tab, const __nv_bfloat16* w,
                              float* hout, __nv_bfloat16* xs, float* red, int c, int G,
-                             float* tmp, const float* mb = nullptr) {
+                             float* tmp, const float* mb = nullptr, int prof_slot = -1) {
   const int d = p.d, tid = threadIdx.x;
+  const bool pe = prof_slot >= 0 && p.prof && c == 0 && tid == 0;
+  if (pe) p.prof[prof_slot] = global_ns();
   float* hs = tmp;                                            // [d] fp32
   __nv_bfloat16* wsm = reinterpret_cast<__nv_bfloat16*>(tmp + d);  // [d] bf16
   float ss = 0.f;
   constexpr int kNB = SR_MK_NB;  // rows per thread per load batch
   const size_t cs = (size_t)p.maxj * kTR;
+  if (mode == 1 && !mb && p.vec_prologue) {
+    // residual + split partials, 4 rows per 16-B load: up to 3 x 512 groups
+    // (d <= 6144) in one batch, i.e. one L2 round trip (rows cut over more
+    // than two CTAs -- small models only -- add a second)
+    constexpr int kG = 3;
+    const int ng = d / 4;
+#pragma unroll 1
+    for (int g0 = tid; g0 < ng; g0 += kG * kMkConsumers) {
+      float4 hb[kG], pa[kG], pq[kG];
+      uint2 wb[kG];
+      int nv[kG];
+#pragma unroll
+      for (int jj = 0; jj < kG; ++jj) {
+        const int gi = g0 + jj * kMkConsumers;
+        const int i = (gi < ng ? gi : 0) * 4;
+        wb[jj] = *reinterpret_cast<const uint2*>(w + i);
+        hb[jj] = __ldcg(reinterpret_cast<const float4*>(hin + i));
+        const int e = tab[i / kTR], r = i % kTR;
+        const int c0 = e & 0xff, n = (e >> 8) & 0xf, j0 = e >> 12;
+        pa[jj] = __ldcg(reinterpret_cast<const float4*>(part + (size_t)c0 * cs + (size_t)j0 * kTR + r));
+        pq[jj] = n > 1 ? __ldcg(reinterpret_cast<const float4*>(part + (size_t)(c0 + 1) * cs + r))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        nv[jj] = gi < ng ? n : 0;
+      }
+#pragma unroll
+      for (int jj = 0; jj < kG; ++jj) {
+        if (nv[jj] == 0) continue;
+        const int i = (g0 + jj * kMkConsumers) * 4;
+        float4 sp = make_float4(pa[jj].x + pq[jj].x, pa[jj].y + pq[jj].y, pa[jj].z + pq[jj].z,
+                                pa[jj].w + pq[jj].w);
+        if (nv[jj] > 2) {
+          const int c0 = tab[i / kTR] & 0xff, r = i % kTR;
+          for (int q = 2; q < nv[jj]; ++q) {
+            const float4 t = __ldcg(reinterpret_cast<const float4*>(part + (size_t)(c0 + q) * cs + r));
+            sp.x += t.x;
+            sp.y += t.y;
+            sp.z += t.z;
+            sp.w += t.w;
+          }
+        }
+        const float4 v = make_float4(hb[jj].x + sp.x, hb[jj].y + sp.y, hb[jj].z + sp.z, hb[jj].w + sp.w);
+        *reinterpret_cast<float4*>(hs + i) = v;
+        *reinterpret_cast<uint2*>(wsm + i) = wb[jj];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+    }
+  } else
 #pragma unroll 1
   for (int i0 = tid; i0 < d; i0 += kNB * kMkConsumers) {
     float hb[kNB], pb[kNB][4];
@@ -281,7 +330,9 @@ SR_DEV void mk_norm_prologue(const MkParams& p, int mode, int tok, const float* 
       }
     }
   }
+  if (pe) p.prof[prof_slot + 1] = global_ns();
   ss = cblock_sum(ss, red);  // (its barriers also publish hs / wsm)
+  if (pe) p.prof[prof_slot + 2] = global_ns();
   const float rstd = rsqrtf(ss / d + p.eps);
   const int dpad = (d + kTC - 1) / kTC * kTC;
   for (int i = tid; i < d; i += kMkConsumers) {
@@ -291,6 +342,7 @@ SR_DEV void mk_norm_prologue(const MkParams& p, int mode, int tok, const float* 
   }
   for (int i = d + tid; i < dpad; i += kMkConsumers) xs[i] = __float2bfloat16_rn(0.f);
   cbar();
+  if (pe) p.prof[prof_slot + 3] = global_ns();
 }
 
 SR_DEV void mk_stage_vec(const __nv_bfloat16* src, int K, __nv_bfloat16* xs) {
@@ -505,6 +557,166 @@ SR_DEV void mma16816(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint3
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
 
+SR_DEV void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+SR_DEV void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Pipelined page loop (two page buffers): warps 0-7 (the S group) run S and
+// the softmax of page k while warps 8-15 (the V group) run P.V of page k - 1.
+//   S group, page k: wait K(k) | S | row max over the group (bar 2) | fetch
+//     K(k+2) into the freed buffer | P(k) hi/lo + alpha(k) into P buffer k&1
+//     (after the V group released it: bar 5 + (k&1)) | arrive bar 3 + (k&1)
+//   V group, page k: sync bar 3 + (k&1) | wait V(k) | O *= alpha(k) | P.V
+//     (warp 8 + v: dims 16v..16v+15) | bar 7 | fetch V(k+2) | arrive bar 5 + (k&1)
+// Each warp of the S group keeps the l partial of its 8 positions (rescaled
+// by alpha like O); they are summed once at the end.
+SR_DEV void mk_attn_pipelined(const MkParams& p, int layer, int g, int pos, const int* page_table,
+                              int p0, int np, bool has_new, int nh, int jl, int c,
+                              uint8_t* const* kvb, uint64_t* kvbar, uint32_t& kvpar,
+                              uint32_t q_addr, uint32_t p_addr, uint32_t lo_off, uint32_t pb_stride,
+                              __nv_bfloat16* pbh, __nv_bfloat16* pbl, float* red_max, float* red_sum,
+                              float* alpha_s, const __nv_bfloat16* knb, const __nv_bfloat16* vnb) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gr = lane >> 2, tq = lane & 3;
+  const float scale = 1.4426950408889634f * 0.08838834764831845f;
+  auto fetch = [&](int k, int which) {
+    const int b = k & 1;
+    mk_fetch_tile(p, which, layer, g, page_table[p0 + k], kvb[b] + which * 2 * kKvTile,
+                  kvbar + 2 * b + which);
+  };
+  uint32_t par = kvpar;
+  float* a_out = p.apart + ((size_t)c * kMkMaxGq + jl + gr) * 130;
+  if (warp < 8) {
+    // ------------------------------------------------------------ S group
+    const int kr = 8 * warp + (lane & 7);
+    float m_run = -INFINITY, l_part = 0.f;
+    for (int k = 0; k < np; ++k) {
+      const int b = k & 1;
+      const int P0 = (p0 + k) * kPage;
+      const int nval = min(kPage, pos + 1 - P0);
+      const bool last = has_new && k == np - 1;
+      uint8_t* kbuf = kvb[b];
+      mbar_wait(kvbar + 2 * b, (par >> (2 * b)) & 1u);
+      par ^= 1u << (2 * b);
+      if (last) {
+        if (tid < kHeadDim / 8)
+          *reinterpret_cast<uint4*>(kbuf + kv_swz(nval - 1, tid)) = reinterpret_cast<const uint4*>(knb)[tid];
+        bar_sync_n(2, 256);
+      }
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint32_t k_smem = smem_u32(kbuf);
+#pragma unroll
+      for (int kk = 0; kk < kHeadDim / 16; kk += 2) {
+        uint32_t a[4], bb[4];
+        ldsm_x4(a, q_addr + kk * 32);
+        ldsm_x4(bb, k_smem + kv_swz(kr, 2 * kk + (lane >> 3)));
+        mma16816(sc, a[0], a[1], bb[0], bb[1]);
+        mma16816(sc, a[2], a[3], bb[2], bb[3]);
+      }
+      const int c0p = 8 * warp + 2 * tq;
+      const float s0 = c0p < nval ? sc[0] * scale : -INFINITY;
+      const float s1 = c0p + 1 < nval ? sc[1] * scale : -INFINITY;
+      float mx = fmaxf(s0, s1);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      float* rm = red_max + b * 64;
+      if (tq == 0) rm[warp * 8 + gr] = mx;
+      bar_sync_n(2, 256);  // K(k) consumed, row maxima in
+      if (tid == 0 && k + 2 < np) fetch(k + 2, 0);
+      float pm = rm[gr];
+#pragma unroll
+      for (int w2 = 1; w2 < 8; ++w2) pm = fmaxf(pm, rm[w2 * 8 + gr]);
+      const float m_new = fmaxf(m_run, pm);
+      const float alpha = exp2f(m_run - m_new);
+      m_run = m_new;
+      const float e0 = exp2f(s0 - m_new), e1 = exp2f(s1 - m_new);
+      const __nv_bfloat16 h0 = __float2bfloat16_rn(e0), h1 = __float2bfloat16_rn(e1);
+      __nv_bfloat162 hi, lo;
+      hi.x = h0;
+      hi.y = h1;
+      lo.x = __float2bfloat16_rn(e0 - __bfloat162float(h0));
+      lo.y = __float2bfloat16_rn(e1 - __bfloat162float(h1));
+      float rs = e0 + e1;
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+      l_part = l_part * alpha + rs;
+      if (k >= 2) bar_sync_n(5 + b, 512);  // the V group is done with P buffer b (page k - 2)
+      *reinterpret_cast<__nv_bfloat162*>(pbh + b * 8 * kPRow + gr * kPRow + c0p) = hi;
+      *reinterpret_cast<__nv_bfloat162*>(pbl + b * 8 * kPRow + gr * kPRow + c0p) = lo;
+      if (warp == 0 && tq == 0) alpha_s[b * 8 + gr] = alpha;
+      bar_arrive_n(3 + b, 512);  // P(k), alpha(k) ready
+    }
+    // consume the V group's last releases (one per page in all)
+    for (int k = np > 2 ? np : 2; k < np + 2; ++k) bar_sync_n(5 + (k & 1), 512);
+    if (tq == 0) red_sum[warp * 8 + gr] = l_part;
+    bar_sync_n(2, 256);
+    if (warp == 0 && tq == 0 && gr < nh) {
+      float l = red_sum[gr];
+#pragma unroll
+      for (int w2 = 1; w2 < 8; ++w2) l += red_sum[w2 * 8 + gr];
+      a_out[128] = m_run;
+      a_out[129] = l;
+    }
+  } else {
+    // ------------------------------------------------------------ V group
+    const int v = warp - 8;
+    const int vr = (lane >> 3) * 8 + (lane & 7);
+    float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int k = 0; k < np; ++k) {
+      const int b = k & 1;
+      const int P0 = (p0 + k) * kPage;
+      const int nval = min(kPage, pos + 1 - P0);
+      const bool last = has_new && k == np - 1;
+      uint8_t* vbuf = kvb[b] + 2 * kKvTile;
+      bar_sync_n(3 + b, 512);  // P(k) ready
+      mbar_wait(kvbar + 2 * b + 1, (par >> (2 * b + 1)) & 1u);
+      par ^= 1u << (2 * b + 1);
+      if (last) {  // new v row; rows past the context zeroed
+        for (int t = tid - 256; t < (kPage - nval + 1) * 16; t += 256) {
+          const int r = nval - 1 + t / 16, q = t % 16;
+          *reinterpret_cast<uint4*>(vbuf + kv_swz(r, q)) =
+              r == nval - 1 ? reinterpret_cast<const uint4*>(vnb)[q] : make_uint4(0, 0, 0, 0);
+        }
+        bar_sync_n(7, 256);
+      }
+      const float alpha = alpha_s[b * 8 + gr];
+#pragma unroll
+      for (int n = 0; n < 2; ++n) {
+        o[n][0] *= alpha;
+        o[n][1] *= alpha;
+      }
+      const uint32_t v_smem = smem_u32(vbuf), pa = p_addr + b * pb_stride;
+#pragma unroll
+      for (int ks = 0; ks < kPage / 16; ks += 2) {
+        uint32_t ah[4], al[4];
+        ldsm_x4(ah, pa + ks * 32);
+        ldsm_x4(al, pa + lo_off + ks * 32);
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          uint32_t bb[4];
+          ldsm_x4t(bb, v_smem + kv_swz(vr + 16 * ks, 2 * v + n));
+          mma16816(o[n], ah[0], ah[1], bb[0], bb[1]);
+          mma16816(o[n], al[0], al[1], bb[0], bb[1]);
+          mma16816(o[n], ah[2], ah[3], bb[2], bb[3]);
+          mma16816(o[n], al[2], al[3], bb[2], bb[3]);
+        }
+      }
+      bar_sync_n(7, 256);  // V(k) and P(k) consumed by the group
+      if (tid == 256 && k + 2 < np) fetch(k + 2, 1);
+      bar_arrive_n(5 + b, 512);  // P buffer b free
+    }
+    if (gr < nh) {
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+        *reinterpret_cast<float2*>(a_out + 16 * v + 8 * n + 2 * tq) = make_float2(o[n][0], o[n][1]);
+    }
+  }
+  // both groups leave with the same barrier phases: buffer b was used by the
+  // pages k = b, b + 2, ...; each use flipped its K and V barrier once
+  const int n0 = (np + 1) / 2, n1 = np / 2;
+  kvpar ^= ((n0 & 1) ? 3u : 0u) | ((n1 & 1) ? 12u : 0u);
+  cbar();
+}
+
 // Attention of kv head g over pages [p0, p1) for its query heads [jl, jh)
 // (<= 8: the MMA's rows 0-7, rows 8-15 zero), on the tensor cores:
 //   S = Q.K^T  warps 0-7, warp w = positions 8w..8w+7 of the page (m16n8k16,
@@ -528,11 +740,12 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
   const int p0 = (int)((long long)npages * s / PS), p1 = (int)((long long)npages * (s + 1) / PS);
   const int jl = Gq * hp / hs, jh = Gq * (hp + 1) / hs, nh = jh - jl;
   __nv_bfloat16* qb = reinterpret_cast<__nv_bfloat16*>(sm);          // [8][kQRow]
-  __nv_bfloat16* pbh = qb + 8 * kQRow;                               // [8][kPRow] P hi
-  __nv_bfloat16* pbl = pbh + 8 * kPRow;                              // [8][kPRow] P lo
-  float* red_max = reinterpret_cast<float*>(pbl + 8 * kPRow);        // [8 warps][8 rows]
-  float* red_sum = red_max + 64;                                     // [8 warps][8 rows]
-  __nv_bfloat16* knb = reinterpret_cast<__nv_bfloat16*>(red_sum + 64);  // [128] new k
+  __nv_bfloat16* pbh = qb + 8 * kQRow;                               // [2][8][kPRow] P hi
+  __nv_bfloat16* pbl = pbh + 2 * 8 * kPRow;                          // [2][8][kPRow] P lo
+  float* red_max = reinterpret_cast<float*>(pbl + 2 * 8 * kPRow);    // [2][8 warps][8 rows]
+  float* red_sum = red_max + 2 * 64;                                 // [8 warps][8 rows]
+  float* alpha_s = red_sum + 64;                                     // [2][8 rows]
+  __nv_bfloat16* knb = reinterpret_cast<__nv_bfloat16*>(alpha_s + 16);  // [128] new k
   __nv_bfloat16* vnb = knb + kHeadDim;                                  // [128] new v
   // page buffer b: K at kvb[b], V at kvb[b] + 2 boxes; mbarriers kvbar[2b] (K),
   // kvbar[2b + 1] (V), phase parity in bit j of kvpar for barrier j.  With
@@ -612,6 +825,13 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
   // (lane >> 3) * 8 + (lane & 7) (+16ks), chunk w (dims 8w..8w+7)
   const int kr = 8 * (warp & 7) + (lane & 7), vr = (lane >> 3) * 8 + (lane & 7);
   const uint32_t p_addr = smem_u32(pbh) + (lane & 7) * kPRow * 2 + (lane >> 3) * 16;
+  const uint32_t lo_off = (uint32_t)(pbl - pbh) * 2, pb_stride = 8 * kPRow * 2;
+  if (dbl) {
+    mk_attn_pipelined(p, layer, g, pos, page_table, p0, np, has_new, nh, jl, c, kvb, kvbar, kvpar,
+                      q_addr, p_addr, lo_off, pb_stride, pbh, pbl, red_max, red_sum, alpha_s, knb, vnb);
+    SUB_EV();
+    return;
+  }
 
   for (int k = 0; k < np; ++k) {
     const int pg_i = p0 + k;
@@ -700,7 +920,7 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
     for (int ks = 0; ks < kPage / 16; ks += 2) {
       uint32_t ah[4], al[4], b[4];
       ldsm_x4(ah, p_addr + ks * 32);
-      ldsm_x4(al, p_addr + 8 * kPRow * 2 + ks * 32);
+      ldsm_x4(al, p_addr + lo_off + ks * 32);
       ldsm_x4t(b, v_smem + kv_swz(vr + 16 * ks, warp));  // positions 16ks..16ks+31, dims 8w..+7
       mma16816(o, ah[0], ah[1], b[0], b[1]);
       mma16816(o, al[0], al[1], b[0], b[1]);
@@ -1017,7 +1237,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
         mk_norm_prologue(p, 0, tok, nullptr, nullptr, s_tab[2], ly.ln1, p.hA, xs, red, c, G, kvtmp);
       else
         mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], ly.ln1, p.hA, xs, red, c, G, kvtmp,
-                         mb_d);
+                         mb_d, l == 1 && tstep < 40 ? 1640 : -1);
       MK_EV();  // 1 qkv prologue
       mk_gemv<PH_QKV>(p, s_ph[PH_QKV], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 2 qkv gemv
@@ -1051,7 +1271,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       const float* mb_o = tp ? mk_tp_exchange(p, p.part_o, s_tab[1], ex, c, G) : nullptr;
       // gate / up
       mk_norm_prologue(p, 1, tok, p.hA, p.part_o, s_tab[1], ly.ln2, p.hB, xs, red, c, G, kvtmp,
-                       mb_o);
+                       mb_o, l == 1 && tstep < 40 ? 1650 : -1);
       MK_EV();  // 11 prologue
       mk_gemv<PH_GU>(p, s_ph[PH_GU], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 12 gu gemv

@@ -240,6 +240,7 @@ struct MkParams {
   int evict_first;           // stream weights with an L2 evict-first policy
   int min_pages;             // attention: minimum K/V pages per split
   int kv_dbl;                // attention pages double-buffered (second buffer in the x region)
+  int vec_prologue;          // norm prologues: 16-B loads, one batch (SR_MK_VECPRO=0: scalar)
   int no_load;               // SR_MK_NOLOAD experiment: stages handed out without loading
                              // weights (times the consumer chain alone; results invalid)
   // tensor parallelism over NVLink peer memory (tp_world > 1): every rank's

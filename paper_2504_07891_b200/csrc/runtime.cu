@@ -287,6 +287,8 @@ struct Model {
     p.stages = mk_pick_stages(p.xs_elems);
     p.kv_dbl = mk_pick_kv_dbl(p.stages, p.xs_elems);
     if (const char* v = getenv("SR_MK_KVDBL")) p.kv_dbl = p.kv_dbl && atoi(v) != 0;
+    p.vec_prologue = 1;
+    if (const char* v = getenv("SR_MK_VECPRO")) p.vec_prologue = atoi(v);
     // L2 prefetch run-ahead beyond the ring (tiles); off by default: measured
     // slower on B200 (the extra HBM traffic delays the latency-bound phases)
     p.l2_ahead = -1;

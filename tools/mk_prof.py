@@ -75,6 +75,10 @@ def main() -> None:
                               "last_split_max": round(max([x / 1e3 for x, f in zip(att, last) if f] or [0]), 2)}
     sub = [x for x in ev[1600:1632] if x > 0]
     out["attn_cta0_steps_us"] = [round((b - a) / 1e3, 2) for a, b in zip(sub, sub[1:])]
+    for name, base in (("qkv_prologue_steps_us", 1640), ("gu_prologue_steps_us", 1650)):
+        st = ev[base:base + 4]
+        if all(x > 0 for x in st):  # loads | block sum | normalise + store
+            out[name] = [round((b - a) / 1e3, 2) for a, b in zip(st, st[1:])]
     out["model"] = a.model
     out["ctx"] = a.ctx
     print(json.dumps(out), flush=True)
