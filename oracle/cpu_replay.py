@@ -77,9 +77,10 @@ class CpuModel:
         return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
 
     @torch.no_grad()
-    def forward(self, start: int, n: int, logits: bool = True) -> int:
-        """``n`` new positions at ``start``.. through every layer (context
-        ``start`` cached), then the LM head of the last row; returns argmax."""
+    def forward(self, start: int, n: int, logits: bool = True, layers: int | None = None) -> int:
+        """``n`` new positions at ``start``.. through every layer (or the
+        first ``layers`` of them: a layer sample) with context ``start``
+        cached, then the LM head of the last row; returns argmax."""
         spec = self.spec
         if start + n > self.max_ctx:
             raise ValueError("context exceeds the replay cache")
@@ -88,7 +89,7 @@ class CpuModel:
         h = self.embed[pos % self.embed.shape[0]].float()
         scale = 1.0 / math.sqrt(hd)
         T = start + n
-        for _ in range(spec.n_layers):
+        for _ in range(spec.n_layers if layers is None else layers):
             x = self._norm(h)
             qkv = (x @ self.wqkv.T + self.bqkv).float()
             q = self._rope(qkv[:, : spec.q_dim].view(n, H, hd), pos).to(torch.bfloat16)
@@ -114,30 +115,72 @@ class CpuModel:
         lg = self._norm(h[-1:]) @ self.lm_head.T
         return int(lg.float().argmax())
 
-    def generate(self, start: int, n_fresh: int, n_gen: int) -> None:
+    def generate(self, start: int, n_fresh: int, n_gen: int, layers: int | None = None,
+                 decode_cap: int | None = None) -> float:
         """A generation call: prefill ``n_fresh`` rows (chunked), then
-        ``n_gen - 1`` decode steps (the first token comes from the prefill)."""
+        ``n_gen - 1`` decode steps (the first token comes from the prefill).
+        Returns the call's seconds; with a sample (``layers`` of the model's
+        layers, at most ``decode_cap`` decode steps spread over the call) the
+        sampled time is scaled back: layer parts by n_layers / layers (every
+        layer streams the same bytes: one random layer is reused), decode by
+        (n_gen - 1) / steps run.  The LM head is always run once per token."""
+        L = self.spec.n_layers
+        lf = 1.0 if layers is None else L / layers
+        t_body = t_head = 0.0
         c0 = 0
         while c0 < n_fresh:
             m = min(PREFILL_CHUNK, n_fresh - c0)
-            self.forward(start + c0, m, logits=(c0 + m == n_fresh))
+            t0 = time.perf_counter()
+            self.forward(start + c0, m, logits=False, layers=layers)
+            t_body += time.perf_counter() - t0
             c0 += m
-        for i in range(max(0, n_gen - 1)):
-            self.forward(start + n_fresh + i, 1)
+        t0 = time.perf_counter()
+        self.forward(start + n_fresh - 1, 1, logits=True, layers=0)  # LM head of the last row
+        t_head += time.perf_counter() - t0
+        total = t_body * lf + t_head
+        nd = max(0, n_gen - 1)
+        run = nd if decode_cap is None else min(nd, decode_cap)
+        if run:
+            t0 = time.perf_counter()
+            for j in range(run):
+                i = j * nd // run  # spread over the call's positions
+                self.forward(start + n_fresh + i, 1, layers=layers)
+            td = time.perf_counter() - t0
+            # each sampled step = body (layer-sampled) + head: scale the body only
+            head1 = t_head
+            body_per = max(0.0, td / run - head1)
+            total += nd * (body_per * lf + head1)
+        return total
 
-    def score(self, start: int, n_fresh: int) -> None:
+    def score(self, start: int, n_fresh: int, layers: int | None = None) -> float:
         """A scoring call: prefill the fresh rows, read the last row's logits."""
-        self.generate(start, n_fresh, 1)
+        return self.generate(start, n_fresh, 1, layers=layers)
 
 
 class CpuReplay:
     """Executes recorded call descriptors ``{"model", "kind", "start",
-    "fresh", "n_gen"}`` on the CPU models of a pair; returns wall seconds."""
+    "fresh", "n_gen"}`` on the CPU models of a pair; returns seconds.
 
-    def __init__(self, specs: dict[str, ModelSpec], max_ctx: int, threads: int | None = None) -> None:
+    ``layer_frac`` / ``decode_cap`` bound the work per call (a sample of the
+    layers and of the decode steps, scaled back as ``CpuModel.generate``
+    states); ``None`` executes every layer and token."""
+
+    def __init__(self, specs: dict[str, ModelSpec], max_ctx: int, threads: int | None = None,
+                 layer_frac: float | None = None, decode_cap: int | None = None) -> None:
         self.threads = threads or host_threads()
         torch.set_num_threads(self.threads)
         self.models = {k: CpuModel(s, max_ctx) for k, s in specs.items()}
+        self.layers = {k: (None if layer_frac is None else max(1, round(s.n_layers * layer_frac)))
+                       for k, s in specs.items()}
+        self.decode_cap = decode_cap
+        self.wall_s = 0.0  # host seconds actually spent
+
+    def sample_text(self) -> str:
+        if all(v is None for v in self.layers.values()) and self.decode_cap is None:
+            return "every layer and token"
+        parts = [f"{k}: {v} of {self.models[k].spec.n_layers} layers" for k, v in self.layers.items()]
+        return ("; ".join(parts) + (f"; <= {self.decode_cap} decode steps per call" if self.decode_cap else "")
+                + " (scaled back per call)")
 
     def warm(self) -> None:
         for m in self.models.values():
@@ -146,9 +189,12 @@ class CpuReplay:
 
     def run(self, call: dict) -> float:
         m = self.models[call["model"]]
+        lay = self.layers[call["model"]]
         t0 = time.perf_counter()
         if call["kind"] == "score":
-            m.score(call["start"], call["fresh"])
+            t = m.score(call["start"], call["fresh"], layers=lay)
         else:
-            m.generate(call["start"], call["fresh"], call["n_gen"])
-        return time.perf_counter() - t0
+            t = m.generate(call["start"], call["fresh"], call["n_gen"], layers=lay,
+                           decode_cap=self.decode_cap)
+        self.wall_s += time.perf_counter() - t0
+        return t
