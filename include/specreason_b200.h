@@ -238,6 +238,20 @@ int sr_tp_peer_attach(void* peer, const uint64_t* h_bases); /* world device poin
 int sr_tp_peer_destroy(void* peer);
 int sr_model_set_tp_peer(void* model, void* peer);
 
+/*
+ * Decode-layout weights (no reference counterpart: an HBM layout choice of
+ * the persistent decode kernel).  h_ptrs: n_layers * 4 + 1 device pointers --
+ * per layer qkv, o, gate/up, down, then the LM head -- each matrix [N][K]
+ * re-stored tile-major: tile (b, k) = rows 32b..32b+31 x columns k*tc..
+ * (tc = min(K, 256)), tiles in (b, k) order, each tile as tc/64 boxes of
+ * [32 rows][64 columns] with the 128-B swizzle applied (16-B chunk j of row r
+ * at r * 128 + ((j ^ (r & 7)) << 4)).  The decode kernel then streams each
+ * 16 KB tile with one contiguous bulk copy and runs its GEMVs on mma.sync.
+ * The row-major weights of sr_model_create stay in use for prefill.  NULL
+ * detaches them (row-major TMA boxes, CUDA-core GEMV).
+ */
+int sr_model_set_decode_tiles(void* model, const uint64_t* h_ptrs);
+
 /* device timings of the last sr_generate / sr_score on this model */
 int sr_last_timing(void* model, sr_timing* h_out);
 

@@ -44,12 +44,29 @@ def first_digit_table(vocab: Vocab, n_rows: int) -> torch.Tensor:
     return out
 
 
+def decode_tiles(w: torch.Tensor) -> torch.Tensor:
+    """A [N][K] bf16 matrix in the persistent decode kernel's tile-major
+    layout (``sr_model_set_decode_tiles``): 32-row x tc-column tiles
+    (tc = min(K, 256)) in (row block, k tile) order, each as tc/64 boxes of
+    [32][64] with the 128-B swizzle applied -- the 16-B chunk j of row r
+    stored at chunk position j ^ (r & 7) -- so a tile is one contiguous 16 KB
+    bulk copy whose shared-memory image ``ldmatrix`` reads conflict free."""
+    N, K = w.shape
+    tc = min(K, 256)
+    if N % 32 or K % tc or tc % 64:
+        raise ValueError(f"decode tiles need N % 32 == 0 and K % {tc} == 0 (got {N} x {K})")
+    x = w.view(N // 32, 32, K // tc, tc // 64, 8, 8).permute(0, 2, 3, 1, 4, 5)
+    r = torch.arange(32, device=w.device)[:, None].expand(32, 8)
+    src = torch.arange(8, device=w.device)[None, :] ^ (r & 7)  # chunk stored at position p
+    return x[:, :, :, r, src, :].contiguous().view(-1)
+
+
 class DeviceModel:
     """One model's weights, K/V page pools, workspace and native handle."""
 
     def __init__(self, spec: ModelSpec, weights: dict[str, torch.Tensor], *, max_pos: int,
                  n_pages: int, max_tokens: int = 256, max_new: int = 256,
-                 device: str | torch.device = "cuda") -> None:
+                 device: str | torch.device = "cuda", decode_layout: bool = True) -> None:
         self.lib = native.load()
         self.spec = spec
         self.device = torch.device(device)
@@ -91,6 +108,15 @@ class DeviceModel:
             native.check("sr_model_create", self.lib.sr_model_create(
                 C.byref(self.desc), C.byref(ptrs), C.c_void_p(stream), C.byref(handle)))
         self.handle = handle
+        # decode-layout copy of the streamed matrices (the row-major weights
+        # stay for prefill): one contiguous bulk copy per 16 KB tile, GEMVs on
+        # the tensor cores (K3)
+        self.tiles: list[torch.Tensor] = []
+        if decode_layout:
+            names = [f"layers.{i}.{n}" for i in range(spec.n_layers) for n in ("wqkv", "wo", "wgu", "wd")]
+            self.tiles = [decode_tiles(W[n]) for n in names + ["lm_head"]]
+            arr = (C.c_uint64 * len(self.tiles))(*(t.data_ptr() for t in self.tiles))
+            native.check("sr_model_set_decode_tiles", self.lib.sr_model_set_decode_tiles(handle, arr))
         self.free_pages = list(range(n_pages - 1, -1, -1))
         self.max_tokens = max_tokens
         # staging

@@ -66,6 +66,7 @@ constexpr int kMkThreads = kMkConsumers + 32;
 constexpr int kTR = 32;                    // tile rows
 constexpr int kTC = 256;                   // tile columns (bf16)
 constexpr int kTileBytes = kTR * kTC * 2;  // 16 KB
+constexpr int kSubTileBytes = kTR * 64 * 2; // one [32][64] swizzled box of a tile-major tile (4 KB)
 #ifndef SR_MK_NB
 #define SR_MK_NB 4
 #endif
@@ -503,6 +504,107 @@ SR_DEV void mk_gemv(const MkParams& p, const PhaseInfo& pi, int c, const uint8_t
   }
 }
 
+
+// Tensor-core form of mk_gemv (p.tiled): the tile arrives (one bulk copy of
+// the tile-major weights) as tc/64 boxes of 32 rows x 64 columns, 128-B swizzled (16-B chunk j of row r at
+// r * 128 + ((j ^ (r & 7)) << 4)).  Warp w owns rows 16*(w & 1) .. +15 and
+// columns 32*(w >> 1) .. +31 of every tile: two m16n8k16 MMAs per tile with
+// the weights as A (ldmatrix.x4) and x as every column of B, so each of the
+// 8 output columns is the same dot product.  The fp32 accumulators run over
+// the row block's k tiles; at its end the 8 column slices of each row are
+// summed in fixed order through shared memory (one barrier per row block,
+// double-buffered) and thread r < 32 finishes row r exactly as mk_gemv does.
+SR_DEV void mma16816f(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int PH>
+SR_DEV void mk_gemv_mma(const MkParams& p, const PhaseInfo& pi, int c, const uint8_t* ring,
+                        uint64_t* full, uint64_t* empty, const __nv_bfloat16* xs, RingPos& rp, int S,
+                        Top2& best, float* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lo = pi.lo, hi = pi.hi, kt = pi.kt, tc = pi.tc;
+  const int mt = warp & 1, ks = warp >> 1;           // row half, 32-column slice
+  const bool active = 32 * ks < tc;
+  const int r16 = 16 * mt + (lane & 15);              // A row this lane addresses
+  const int sub = ks >> 1, ch0 = (ks & 1) * 4 + (lane >> 4);
+  // byte offset in a tile of (row r16, chunk ch0 + 2 * step) for steps 0, 1
+  const uint32_t a_off0 = sub * kSubTileBytes + r16 * 128 + (((ch0) ^ (r16 & 7)) << 4);
+  const uint32_t a_off1 = sub * kSubTileBytes + r16 * 128 + (((ch0 + 2) ^ (r16 & 7)) << 4);
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t xs_s = smem_u32(xs) + (32 * ks + 2 * (lane & 3)) * 2;
+  const int g = lane >> 2;
+  int b = pi.b0, k = pi.k0, blk = 0;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int u0 = lo; u0 < hi; u0 += kUPS) {
+    mbar_wait(&full[rp.slot], rp.par);
+    const uint32_t stage = ring_s + rp.slot * kStageBytes;
+    const int nu = hi - u0 < kUPS ? hi - u0 : kUPS;
+#pragma unroll
+    for (int q = 0; q < kUPS; ++q) {
+      if (q < nu) {
+        const int u = u0 + q;
+        if (active) {
+          const uint32_t t = stage + q * kTileBytes;
+          uint32_t a0[4], a1[4], x0, x1, x2, x3;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(a0[0]), "=r"(a0[1]), "=r"(a0[2]), "=r"(a0[3]) : "r"(t + a_off0));
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(a1[0]), "=r"(a1[1]), "=r"(a1[2]), "=r"(a1[3]) : "r"(t + a_off1));
+          const uint32_t xa = xs_s + k * tc * 2;
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x0) : "r"(xa));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x1) : "r"(xa + 16));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x2) : "r"(xa + 32));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x3) : "r"(xa + 48));
+          mma16816f(acc, a0, x0, x1);
+          mma16816f(acc, a1, x2, x3);
+        }
+        if (q == nu - 1) {  // stage fully read: hand it back to the producer
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[rp.slot]);
+          rp.advance(S);
+        }
+        if (k == kt - 1 || u == hi - 1) {
+          float* rb = red + (blk & 1) * 256;  // [8 slices][32 rows]
+          if ((lane & 3) == 0) {
+            rb[ks * 32 + 16 * mt + g] = acc[0];
+            rb[ks * 32 + 16 * mt + g + 8] = acc[2];
+          }
+          cbar();
+          if (warp == 0) {
+            float v = rb[lane];
+#pragma unroll
+            for (int s2 = 1; s2 < 8; ++s2) v += rb[s2 * 32 + lane];
+            if constexpr (PH == PH_QKV || PH == PH_O || PH == PH_D) {
+              float* part = PH == PH_QKV ? p.part_qkv : PH == PH_O ? p.part_o : p.part_d;
+              part[((size_t)c * p.maxj + (b - pi.b0)) * kTR + lane] = v;
+            } else if constexpr (PH == PH_GU) {
+              const float up = __shfl_down_sync(0xffffffffu, v, 16);
+              if (lane < 16) p.act[b * 16 + lane] = __float2bfloat16_rn(v / (1.f + __expf(-v)) * up);
+            } else {
+              const int r = b * kTR + lane;
+              if (r < p.vocab_text) best.push(v, r);
+            }
+          }
+          ++blk;
+          acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+        }
+        if (++k == kt) {
+          k = 0;
+          ++b;
+        }
+      }
+    }
+  }
+  // LM head: warp 0's lanes each tracked their own rows; lane 0 reports the merge
+  if constexpr (PH == PH_LM) {
+    if (warp == 0) warp_top2(best);
+  }
+}
 
 SR_DEV float mk_qkv_val(const MkParams& p, const __nv_bfloat16* bias, const uint16_t* tab,
                         int row) {
@@ -1004,10 +1106,12 @@ SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, int hs, float* 
 struct MkCursor {
   int l, k, u, hi, kk, bb, kt, tc, bytes;
   const CUtensorMap* map;
+  const uint8_t* tbase;  // tile-major weights of the phase (p.tiled)
   SR_DEV void enter(const MkParams& p, const PhaseInfo* ph) {
     for (;;) {
       const PhaseInfo& pi = ph[l < p.L ? k : PH_LM];
       map = p.maps + (l < p.L ? l * 4 + k : p.L * 4);
+      tbase = p.tiled ? static_cast<const uint8_t*>(p.tiles[l < p.L ? l * 4 + k : p.L * 4]) : nullptr;
       u = pi.lo;
       hi = pi.hi;
       kk = pi.k0;
@@ -1040,6 +1144,7 @@ struct MkCursor {
   }
   SR_DEV int col() const { return kk * tc; }
   SR_DEV int row() const { return bb * kTR; }
+  SR_DEV const uint8_t* tile() const { return tbase + ((size_t)bb * kt + kk) * bytes; }
 };
 
 SR_DEV void l2_prefetch(const void* ptr, uint32_t bytes) {
@@ -1072,6 +1177,10 @@ SR_DEV void mk_prefetch_next_layer(const MkParams& p, int l, int pos, const int*
   }
 }
 
+// kTiled: the tile-major weights + mma.sync consumers (p.tiled), else row-major
+// TMA boxes + CUDA-core consumers; two instantiations, so each carries the
+// registers of one consumer only
+template <bool kTiled>
 __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams p) {
   extern __shared__ __align__(1024) uint8_t mk_smem[];
   __shared__ __align__(8) uint64_t full[kMkMaxStages];
@@ -1081,6 +1190,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   __shared__ int s_i1[kMkWarps];
   __shared__ int s_tok;
   __shared__ uint16_t s_tab[3][kMkTab];  // contributor tables: qkv, o, down
+  __shared__ float s_gred[2 * 256];       // mma GEMV: per-row-block slice sums, 2 buffers
   __shared__ PhaseInfo s_ph[5];
   __shared__ __align__(8) uint64_t kvbar[4];  // K, V of page buffer 0; K, V of buffer 1
   __shared__ float s_margin, s_rv1, s_rv2;
@@ -1156,7 +1266,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
             mbar_expect_tx(&full[slot], nu * ld.bytes);
             uint8_t* dst = ring + (size_t)slot * kStageBytes;
             for (int q = 0; q < nu; ++q) {
-              if (p.evict_first)
+              if (kTiled)  // one contiguous 16 KB tile, already in the smem image
+                bulk_load_1d_hint(dst + q * kTileBytes, ld.tile(), ld.bytes, &full[slot], pol);
+              else if (p.evict_first)
                 tma_load_2d_hint(dst + q * kTileBytes, ld.map, &full[slot], ld.col(), ld.row(), pol);
               else
                 tma_load_2d(dst + q * kTileBytes, ld.map, &full[slot], ld.col(), ld.row());
@@ -1242,7 +1354,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
         mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], ly.ln1, p.hA, xs, red, c, G, kvtmp,
                          mb_d, l == 1 && tstep < 40 ? 1640 : -1);
       MK_EV();  // 1 qkv prologue
-      mk_gemv<PH_QKV>(p, s_ph[PH_QKV], c, ring, full, empty, xs, rp, S, best);
+      if constexpr (kTiled) mk_gemv_mma<PH_QKV>(p, s_ph[PH_QKV], c, ring, full, empty, xs, rp, S, best, s_gred); else mk_gemv<PH_QKV>(p, s_ph[PH_QKV], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 2 qkv gemv
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 3 sync
@@ -1267,7 +1379,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       // O
       mk_stage_vec(p.attn, p.q_dim, xs);
       MK_EV();  // 8 stage
-      mk_gemv<PH_O>(p, s_ph[PH_O], c, ring, full, empty, xs, rp, S, best);
+      if constexpr (kTiled) mk_gemv_mma<PH_O>(p, s_ph[PH_O], c, ring, full, empty, xs, rp, S, best, s_gred); else mk_gemv<PH_O>(p, s_ph[PH_O], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 9 o gemv
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 10 sync
@@ -1276,14 +1388,14 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       mk_norm_prologue(p, 1, tok, p.hA, p.part_o, s_tab[1], ly.ln2, p.hB, xs, red, c, G, kvtmp,
                        mb_o, l == 1 && tstep < 40 ? 1650 : -1);
       MK_EV();  // 11 prologue
-      mk_gemv<PH_GU>(p, s_ph[PH_GU], c, ring, full, empty, xs, rp, S, best);
+      if constexpr (kTiled) mk_gemv_mma<PH_GU>(p, s_ph[PH_GU], c, ring, full, empty, xs, rp, S, best, s_gred); else mk_gemv<PH_GU>(p, s_ph[PH_GU], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 12 gu gemv
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 13 sync
       // down
       mk_stage_vec(p.act, p.f, xs);
       MK_EV();  // 14 stage
-      mk_gemv<PH_D>(p, s_ph[PH_D], c, ring, full, empty, xs, rp, S, best);
+      if constexpr (kTiled) mk_gemv_mma<PH_D>(p, s_ph[PH_D], c, ring, full, empty, xs, rp, S, best, s_gred); else mk_gemv<PH_D>(p, s_ph[PH_D], c, ring, full, empty, xs, rp, S, best);
       MK_EV();  // 15 down gemv
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 16 sync
@@ -1293,7 +1405,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
     mk_norm_prologue(p, 1, tok, p.hB, p.part_d, s_tab[2], p.ln_f, nullptr, xs, red, c, G, kvtmp,
                      mb_d);
     MK_EV();
-    mk_gemv<PH_LM>(p, s_ph[PH_LM], c, ring, full, empty, xs, rp, S, best);
+    if constexpr (kTiled) mk_gemv_mma<PH_LM>(p, s_ph[PH_LM], c, ring, full, empty, xs, rp, S, best, s_gred); else mk_gemv<PH_LM>(p, s_ph[PH_LM], c, ring, full, empty, xs, rp, S, best);
     MK_EV();
     if (lane == 0) {
       s_v1[warp] = best.v1;
@@ -1392,13 +1504,13 @@ size_t mk_smem_bytes(int stages, int xs_elems, int kv_dbl) {
 
 int mk_pick_stages(int xs_elems) {
   int s = kMkMaxStages;
-  while (s > 2 && mk_smem_bytes(s, xs_elems, 0) > 225 * 1024) --s;
+  while (s > 2 && mk_smem_bytes(s, xs_elems, 0) > 222 * 1024) --s;  // + <= 5 KB static
   return s;
 }
 
 // double-buffer the attention pages when that costs no ring stage
 int mk_pick_kv_dbl(int stages, int xs_elems) {
-  return mk_smem_bytes(stages, xs_elems, 1) <= 225 * 1024 ? 1 : 0;
+  return mk_smem_bytes(stages, xs_elems, 1) <= 222 * 1024 ? 1 : 0;
 }
 
 int mk_max_j(int N, int K, int num_sms) {
@@ -1415,8 +1527,10 @@ cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream) {
   const size_t smem = mk_smem_bytes(p.stages, p.xs_elems, p.kv_dbl);
   static size_t attr = 0;
   if (attr < smem) {
-    cudaError_t e =
-        cudaFuncSetAttribute(decode_mk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_mk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(decode_mk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
@@ -1430,7 +1544,8 @@ cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, decode_mk_kernel, p);
+  return p.tiled ? cudaLaunchKernelEx(&cfg, decode_mk_kernel<true>, p)
+                 : cudaLaunchKernelEx(&cfg, decode_mk_kernel<false>, p);
 }
 
 }  // namespace sr

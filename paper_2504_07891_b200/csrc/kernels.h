@@ -241,6 +241,12 @@ struct MkParams {
   int min_pages;             // attention: minimum K/V pages per split
   int kv_dbl;                // attention pages double-buffered (second buffer in the x region)
   int vec_prologue;          // norm prologues: 16-B loads, one batch (SR_MK_VECPRO=0: scalar)
+  // tile-major decode weights (sr_model_set_decode_tiles): per layer qkv, o,
+  // gate/up, down, then the LM head; tile (b, k) of a matrix is 32 rows x tc
+  // columns at ((b * kt) + k) * 32 * tc * 2 bytes, stored as tc / 64 boxes of
+  // [32][64] with the 128-B swizzle applied; null = row-major + TMA 2-D boxes
+  const void* const* tiles;
+  int tiled;                 // 1: stream tiles by 1-D bulk copy, GEMV on mma.sync
   int no_load;               // SR_MK_NOLOAD experiment: stages handed out without loading
                              // weights (times the consumer chain alone; results invalid)
   // tensor parallelism over NVLink peer memory (tp_world > 1): every rank's

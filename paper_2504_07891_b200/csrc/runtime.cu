@@ -45,7 +45,7 @@ constexpr int kAttnItemsMax = 4096;  // (span, query tile) items of one multi-se
 
 struct Layout {  // workspace carve-up (byte offsets)
   size_t st, h, x, q, attn, act, part, apart, actr, lm_v1, lm_v2, lm_i1, lm_ctr, logits, ro_cnt,
-      mk_maps, mk_layers, mk_h, mk_part, mk_apart, mk_lm, mk_prof, mk_ctab, tp_delta, tp_small, attn_items, attn_tabs,
+      mk_maps, mk_layers, mk_tiles, mk_h, mk_part, mk_apart, mk_lm, mk_prof, mk_ctab, tp_delta, tp_small, attn_items, attn_tabs,
       total;
   int mk_maxj;
   int mk_g;  // CTAs of the persistent decode kernel
@@ -102,6 +102,7 @@ static Layout make_layout(const sr_model_desc& d, int num_sms) {
                         mk_max_j(d.d_model, d.d_ffn, mk_g)});
   L.mk_maps = take(((size_t)d.n_layers * 4 + 3) * sizeof(CUtensorMap));  // + K, V pools
   L.mk_layers = take((size_t)d.n_layers * sizeof(MkLayer));
+  L.mk_tiles = take(((size_t)d.n_layers * 4 + 1) * sizeof(void*));  // tile-major weight pointers
   L.mk_h = take(2 * (size_t)d.d_model * 4);
   L.mk_part = take(3 * (size_t)mk_g * L.mk_maxj * mk_tile_rows() * 4);
   L.mk_apart = take((size_t)num_sms * 8 * 130 * 4);
@@ -287,6 +288,8 @@ struct Model {
     p.stages = mk_pick_stages(p.xs_elems);
     p.kv_dbl = mk_pick_kv_dbl(p.stages, p.xs_elems);
     if (const char* v = getenv("SR_MK_KVDBL")) p.kv_dbl = p.kv_dbl && atoi(v) != 0;
+    p.tiles = nullptr;
+    p.tiled = 0;
     p.vec_prologue = 1;
     if (const char* v = getenv("SR_MK_VECPRO")) p.vec_prologue = atoi(v);
     // L2 prefetch run-ahead beyond the ring (tiles); off by default: measured
@@ -1372,6 +1375,29 @@ int sr_model_set_tp_peer(void* model, void* peer) {
   for (int q = 0; q < kPeerMaxWorld; ++q) p.tp_base[q] = q < pc->world ? pc->base[q] : nullptr;
   p.tp_off_dec = pc->off_dec;
   p.tp_off_lm = pc->off_lm;
+  return 0;
+}
+
+int sr_model_set_decode_tiles(void* model, const uint64_t* h_ptrs) {
+  Model* m = (Model*)model;
+  if (!m) return fail(SR_E_INVALID, "null model");
+  if (!h_ptrs) {
+    m->mk.tiled = 0;
+    return 0;
+  }
+  const int n = m->d.n_layers * 4 + 1;
+  for (int i = 0; i < n; ++i)
+    if (!h_ptrs[i] || (h_ptrs[i] & 15)) return fail(SR_E_INVALID, "tile-major weight pointer null or not 16-B aligned");
+  // every tile's column count must be a multiple of 64 (the [32][64] boxes)
+  const int K[4] = {m->d.d_model, m->q_dim, m->d.d_model, m->d.d_ffn};
+  for (int i = 0; i < 4; ++i) {
+    const int tc = std::min(K[i], mk_tile_cols());
+    if (tc % 64 || K[i] % tc) return fail(SR_E_INVALID, "tile-major decode needs K % 64 == 0 and K % tile == 0");
+  }
+  SR_CK(cudaMemcpy(m->ws + m->L.mk_tiles, h_ptrs, n * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  m->mk.tiles = reinterpret_cast<const void* const*>(m->ws + m->L.mk_tiles);
+  m->mk.tiled = 1;
+  if (const char* v = getenv("SR_MK_TILED")) m->mk.tiled = atoi(v) != 0;
   return 0;
 }
 

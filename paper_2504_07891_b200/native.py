@@ -78,6 +78,7 @@ EXPORTS = {
     "sr_tp_peer_attach": (C.c_int, [C.c_void_p, C.c_void_p]),
     "sr_tp_peer_destroy": (C.c_int, [C.c_void_p]),
     "sr_model_set_tp_peer": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sr_model_set_decode_tiles": (C.c_int, [C.c_void_p, C.c_void_p]),
 }
 
 _lib = None
