@@ -38,12 +38,15 @@ def main() -> None:
     s = b.pool.streams[0]
     eng.forward_logits(s, ctx, all_rows=False)
     times = []
-    for _ in range(a.reps):
-        ids = torch.randint(16, spec.vocab_text, (a.m,), generator=g).tolist()
-        eng.score(s, ids, 7)
-        t = eng.model.timing()
-        times.append(t.prefill_ms)
-        eng.truncate(s, a.ctx)
+    from bench import ClockSampler  # nvidia-smi clocks / throttle reasons during the timed calls
+
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(a.reps):
+            ids = torch.randint(16, spec.vocab_text, (a.m,), generator=g).tolist()
+            eng.score(s, ids, 7)
+            t = eng.model.timing()
+            times.append(t.prefill_ms)
+            eng.truncate(s, a.ctx)
     ms = min(times)
     P = spec.body_params() + spec.head_params()
     C, M = a.ctx, a.m
@@ -52,7 +55,9 @@ def main() -> None:
         + 2 * spec.vocab_rows * spec.d_model
     print(json.dumps({"model": a.model, "ctx": C, "m": M, "ms": round(ms, 3), "all_ms": [round(x, 3) for x in times],
                       "GBps": round(byts / (ms * 1e-3) / 1e9, 1), "TFLOPs": round(flops / (ms * 1e-3) / 1e12, 1),
-                      "hbm_floor_ms": round(byts / 6552e9 * 1e3, 3)}), flush=True)
+                      "hbm_floor_ms": round(byts / 6552e9 * 1e3, 3),
+                      "tensor_floor_ms": round(flops / 1.374e15 * 1e3, 3),
+                      "clocks": clk.summary()}), flush=True)
 
 
 if __name__ == "__main__":
