@@ -1068,15 +1068,32 @@ SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, int hs, float* 
     int hp = 0;
     while (hp + 1 < hs && Gq * (hp + 1) / hs <= j) ++hp;
     float m = -INFINITY, l = 0.f, o = 0.f;
-    for (int q = grp * hs + hp; q < S_a; q += kMkWarps * hs) {
-      const float* a = p.apart + ((size_t)(g * S_a + q) * kMkMaxGq + j) * 130;
-      const float ms = __ldcg(a + 128), ls = __ldcg(a + 129), os = __ldcg(a + d);
-      if (ms == -INFINITY) continue;  // a head-split CTA's slot for a head it does not own
-      const float mn = fmaxf(m, ms);
-      const float x = exp2f(m - mn), y = exp2f(ms - mn);
-      l = l * x + ls * y;
-      o = o * x + os * y;
-      m = mn;
+    // this group's splits q0, q0 + qs, ...: four at a time, all loads issued
+    // before the (in-order, so unchanged) merge -- one L2 round trip per 4
+    const int q0 = grp * hs + hp, qs = kMkWarps * hs;
+    for (int qb = q0; qb < S_a; qb += 4 * qs) {
+      float ms[4], ls[4], os[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int q = qb + i * qs;
+        ms[i] = -INFINITY;
+        ls[i] = os[i] = 0.f;
+        if (q < S_a) {
+          const float* a = p.apart + ((size_t)(g * S_a + q) * kMkMaxGq + j) * 130;
+          ms[i] = __ldcg(a + 128);
+          ls[i] = __ldcg(a + 129);
+          os[i] = __ldcg(a + d);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (ms[i] == -INFINITY) continue;  // past S_a, or a head-split slot of another head
+        const float mn = fmaxf(m, ms[i]);
+        const float x = exp2f(m - mn), y = exp2f(ms[i] - mn);
+        l = l * x + ls[i] * y;
+        o = o * x + os[i] * y;
+        m = mn;
+      }
     }
     r_o[grp * 32 + dl] = o;
     if (dl == 0) {
