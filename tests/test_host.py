@@ -217,3 +217,24 @@ def test_native_errors_map_onto_the_reference_hierarchy(tiny_vocab):
     t = ModelBackend(Failing(1004), tiny_vocab, prof)
     with pytest.raises(contract.TransportError):
         t.score_step(VerificationRequest("a", "b ", "c "))
+
+
+def test_decode_tiles_layout():
+    """The decode kernel's tile-major weight copy (``backend.decode_tiles``,
+    ``sr_model_set_decode_tiles``): tile (b, k) = rows 32b.. x columns k*tc..
+    in (b, k) order, each as tc/64 boxes of [32][64] whose 16-B chunk j of
+    row r sits at chunk position j ^ (r & 7)."""
+    import torch
+
+    from paper_2504_07891_b200.backend import decode_tiles
+
+    for N, K in ((64, 512), (96, 128), (32, 256), (32, 768)):
+        w = torch.randn(N, K).to(torch.bfloat16)
+        tc = min(K, 256)
+        t = decode_tiles(w).view(N // 32, K // tc, tc // 64, 32, 8, 8)
+        b, r, c = torch.meshgrid(torch.arange(N // 32), torch.arange(32), torch.arange(K), indexing="ij")
+        k, cc = c // tc, c % tc
+        got = t[b, k, cc // 64, r, ((cc % 64) // 8) ^ (r & 7), cc % 8]
+        assert torch.equal(got, w.view(N // 32, 32, K))
+    with pytest.raises(ValueError):
+        decode_tiles(torch.zeros(48, 256, dtype=torch.bfloat16))  # rows not a multiple of 32
