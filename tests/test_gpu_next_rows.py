@@ -156,3 +156,35 @@ def test_f3_prefix_sharing_template_trajectory(c2):
         _clean(replay(be, be.calls, tol(name)))
     print(json.dumps({"f3": {"steps": len(res.state.retained_steps),
                              "mean_fresh_verify_rows": round(sum(fresh) / len(fresh), 1)}}))
+
+
+def test_f4_reference_sweep_on_b200(cuda, stepspec, tmp_path):
+    """f-4 on the device: the reference's own experiment harness
+    (``stepspec.bench.run_sweep``, ``bench.py:221-300``) drives the tiny B200
+    pair and writes ``results.csv`` / ``summary.json`` / traces in the
+    reference schema (``bench.py:25-39``, ``366-407``), after the reference
+    ``profile`` verb's two-point fits (``cli.py:399-442``) measured the
+    backends; threshold 0 accepts every step, 10 rejects every step
+    (``test_acceptance.py:116-126``)."""
+    import csv
+    import sys
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    import sweep
+
+    from paper_2504_07891_b200.backend import build_pair
+    from paper_2504_07891_b200.host import reference_types
+
+    small, base = build_pair("tiny", types=reference_types(stepspec), max_ctx=1024)
+    a = sweep.parse(["--values", "0,7,10", "--tasks", "2", "--length", "2", "--budget", "96",
+                     "--max-step-tokens", "16", "--out", str(tmp_path)])
+    out = sweep.run_with(a, small, base)
+    assert out["records"] == 2 * 3 * 2  # tasks x values x schemes (SpecReason, BaseOnly)
+    rows = [r for r in csv.reader((tmp_path / "results.csv").read_text().splitlines()[1:])]
+    assert rows[0][:3] == ["scheme", "knob", "knob_value"]
+    cells = {(r[0], r[2]): r for r in rows[1:]}
+    assert float(cells[("SpecReason", "0")][8]) == 1.0
+    assert float(cells[("SpecReason", "10")][8]) == 0.0
+    assert json.loads((tmp_path / "summary.json").read_text())["schema"] == "stepspec.results.v1"
+    prof = json.loads((tmp_path / "profiles.json").read_text())
+    assert all(p["decode_s_per_token"] > 0 and p["prefill_tokens_per_s"] > 0 for p in prof.values())
