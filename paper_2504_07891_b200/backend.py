@@ -185,18 +185,25 @@ class EngineStats:
         self.calls += 1
         self.prefill_ms += t.prefill_ms
         self.decode_ms += t.decode_ms
-        self.prefill_tokens += n_ids
-        steps = max(0, n_gen - 1)
-        self.decode_tokens += steps
-        b, f = spec.prefill_cost(start, n_ids, 1, m.max_tokens)
-        self.prefill_bytes += b
-        self.prefill_flops += f
-        ctx0 = start + n_ids
-        for i in range(steps):
-            self.decode_bytes += spec.decode_bytes(ctx0 + i)
-        # decode_begin + prefill + first-token LM head + one persistent decode
-        # kernel for the whole step (decode_mk.cu)
-        self.launches += self._prefill_launches(spec, n_ids) + 3
+        if t.prefill_tokens == 0:  # one fed token: every new token is a decode step
+            steps = n_gen
+            self.decode_tokens += steps
+            for i in range(steps):
+                self.decode_bytes += spec.decode_bytes(start + i)
+            self.launches += 2  # decode_begin + the persistent decode kernel
+        else:
+            self.prefill_tokens += n_ids
+            steps = max(0, n_gen - 1)
+            self.decode_tokens += steps
+            b, f = spec.prefill_cost(start, n_ids, 1, m.max_tokens)
+            self.prefill_bytes += b
+            self.prefill_flops += f
+            ctx0 = start + n_ids
+            for i in range(steps):
+                self.decode_bytes += spec.decode_bytes(ctx0 + i)
+            # decode_begin + prefill + first-token LM head + one persistent
+            # decode kernel for the whole step (decode_mk.cu)
+            self.launches += self._prefill_launches(spec, n_ids) + 3
         self.h2d_bytes += 4 * n_ids + 64
         self.d2h_bytes += 4 * (2 + m.max_new) * 2
 

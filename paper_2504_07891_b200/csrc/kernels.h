@@ -307,7 +307,8 @@ cudaError_t tp_readout_final_launch(const float* dig, int* counts, const float* 
                                     sr_readout* out, cudaStream_t s);
 
 // decode-loop bookkeeping kernels
-cudaError_t decode_begin_launch(DecodeState* st, const DecodeState* h_init, cudaStream_t stream);
+cudaError_t decode_begin_launch(DecodeState* st, const DecodeState* h_init, cudaStream_t stream,
+                                const int32_t* feed = nullptr);
 cudaError_t cond_init_launch(DecodeState* st, unsigned long long handle, cudaStream_t stream);
 
 }  // namespace sr

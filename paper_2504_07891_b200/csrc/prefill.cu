@@ -532,10 +532,14 @@ cudaError_t readout_launch(const ReadoutParams& p, int num_sms, cudaStream_t str
 }
 
 // ===================================================== decode bookkeeping ===
-__global__ void decode_begin_kernel(DecodeState* st, DecodeState init) { *st = init; }
+__global__ void decode_begin_kernel(DecodeState* st, DecodeState init, const int32_t* feed) {
+  if (feed) init.token = feed[0];  // one fed token: the decode kernel processes it itself
+  *st = init;
+}
 
-cudaError_t decode_begin_launch(DecodeState* st, const DecodeState* h_init, cudaStream_t stream) {
-  decode_begin_kernel<<<1, 1, 0, stream>>>(st, *h_init);
+cudaError_t decode_begin_launch(DecodeState* st, const DecodeState* h_init, cudaStream_t stream,
+                                const int32_t* feed) {
+  decode_begin_kernel<<<1, 1, 0, stream>>>(st, *h_init, feed);
   return cudaGetLastError();
 }
 

@@ -155,6 +155,7 @@ struct Model {
   bool attn_simt = false;      // SR_ATTN=simt: CUDA-core split-KV attention (A/B reference)
   bool attn_umma = true;       // tcgen05 prefill attention; SR_ATTN=tc: mma.sync (A/B)
   bool prefetch = false;       // SR_PREFETCH=1: GEMV L2 prefetch before the PDL wait
+  bool feed1 = true;           // one fed token decodes in the persistent kernel (SR_FEED1=0: prefill)
   struct alignas(64) TMap { CUtensorMap m; };
   std::vector<TMap> wmaps;     // per layer: qkv, o, gu, d ; then lm_head
   TMap amaps[3][5];            // [x | attn | act][token tile 32/64/96/128/256]
@@ -897,6 +898,7 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
     m->attn_umma = strcmp(v, "tc") != 0 && !m->attn_simt;
   }
   if (const char* v = getenv("SR_PREFETCH")) m->prefetch = v[0] == '1';
+  if (const char* v = getenv("SR_FEED1")) m->feed1 = v[0] != '0';
   if (const char* v = getenv("SR_ATTN_PHI")) m->p_hi_only = v[0] == '1';
   if (const char* v = getenv("SR_WATCH")) {
     m->watch_on = atoi(v) > 0;
@@ -953,6 +955,20 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
   init.margins = margins;
   init.cond_handle = 0;
   SR_CK(cudaEventRecord(m->ev[0], s));
+  // a single fed token (the stream already holds the rest of the prompt, e.g.
+  // the next step of the same generator) is a decode step: the persistent
+  // kernel feeds it at start_pos and emits the first new token itself, instead
+  // of a prefill pass through the GEMM path (one weight pass either way, the
+  // decode kernel's at ~90 % of HBM rate)
+  if (n_ids == 1 && m->feed1 && !m->tp_on() && !m->stream_decode && !m->graph_decode) {
+    SR_CK(decode_begin_launch(m->st, &init, s, ids));
+    SR_CK(cudaEventRecord(m->ev[1], s));
+    SR_CK(mk_launch(m->mk, m->L.mk_g, s));
+    SR_CK(cudaEventRecord(m->ev[2], s));
+    m->timing.prefill_tokens = 0;
+    m->timing.decode_tokens = 0;  // filled from the output header by the caller
+    return 0;
+  }
   SR_CK(decode_begin_launch(m->st, &init, s));
   int rows = 0;
   int rc = m->prefill(page_table, start_pos, ids, n_ids, s, &rows);
