@@ -1,23 +1,17 @@
-// K4 / K7: paged GQA flash attention on the tensor cores (mma.sync m16n8k16,
-// bf16 in, fp32 accumulate), one kernel for decode and prefill.
+// K4: paged GQA flash attention on the tensor cores (mma.sync m16n8k16, bf16
+// in, fp32 accumulate) for the per-kernel decode paths -- the decode graph
+// (SR_DECODE=graph, the A/B reference of the persistent kernel) and the
+// NCCL tensor-parallel decode loop -- plus the split merge that the prefill
+// attention (attention_umma.cu) uses.
 //
-// Query rows are (token, head-in-group) pairs of one KV head: row r = token
-// r / G, head g*G + r % G, so the G heads sharing a KV head form the MMA's M
-// dimension and every K/V byte is read once per 64-row query tile.
-//
-// CTA = (kv head, KV split, 64-row query tile); 4 warps.  K and V tiles are
-// one page (64 positions x 128 dims bf16 = 16 KB each, contiguous in the page
-// pool) staged by cp.async into a 2-deep ring with a 16-byte-chunk XOR
-// swizzle so ldmatrix is conflict-free.  Each warp owns 16 query rows and
-// runs S = Q K^T (8 n-tiles x 8 k-steps), an exp2 online softmax in
-// registers, P (re-packed to bf16 A fragments, FA2-style) and O += P V
-// (ldmatrix.trans on V).
-//   decode  (M rows <= 16): the 4 warps split the KV tiles of the CTA among
-//           themselves and merge (m, l, O) through shared memory;
-//   prefill (M rows > 16): the 4 warps own 4 row tiles and share KV tiles;
-//           causality: row r sees positions <= start_pos + r / G.
-// With several KV splits per (kv head, query tile) each CTA writes a partial
-// (m, l, O) and the last CTA (atomic ticket) merges them.
+// Query rows are (token, head-in-group) pairs of one KV head, so the G heads
+// sharing a KV head form the MMA's M dimension and every K/V byte is read
+// once.  K and V pages (64 positions x 128 dims bf16 = 16 KB each) are staged
+// by cp.async into a 2-deep ring with a 16-byte-chunk XOR swizzle so ldmatrix
+// is conflict-free; S = Q K^T, an exp2 online softmax in registers, P
+// re-packed to bf16 A fragments (FA2-style) and O += P V (ldmatrix.trans on
+// V).  A cluster of CTAs splits the KV pages of one kv head and merges
+// (m, l, O) through distributed shared memory.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -25,8 +19,6 @@
 
 namespace sr {
 
-constexpr int kTcaThreads = 128;
-constexpr int kRowsPerCta = 64;
 constexpr int kTile = kPage;                // 64 positions per KV tile
 constexpr int kTileBytes = kTile * kHeadDim * 2;  // 16 KB
 constexpr int kAttnMaxSplit = 64;
@@ -63,256 +55,16 @@ SR_DEV void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-struct TcaSmem {
-  __align__(128) uint8_t k[2][kTileBytes];
-  __align__(128) uint8_t v[2][kTileBytes];
-  __align__(128) uint8_t q[kRowsPerCta * kHeadDim * 2];
-};
-
 // Per-warp flash state for 16 query rows (thread holds rows g and g+8).
 struct Flash {
   float o[16][4];   // 16 dim n-tiles x {row g: c0,c1 ; row g+8: c2,c3}
   float m[2], l[2];
 };
 
-template <bool CAUSAL, bool PLO = true>
-SR_DEV void flash_tile(Flash& F, const uint32_t (&qa)[8][4], uint32_t ks, uint32_t vs, int lane,
-                       int tile_pos0, int lim0, int lim1) {
-  // S = Q K^T for 16 rows x 64 positions
-  float s[8][4];
-#pragma unroll
-  for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
-#pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {      // 16-dim k-steps
-#pragma unroll
-    for (int np = 0; np < 4; ++np) {    // pairs of 8-position n-tiles
-      // x4: (pos 0-7, dims kk*16+0..7), (pos 0-7, +8..15), (pos 8-15, +0..7), (pos 8-15, +8..15)
-      const int row = np * 16 + ((lane >> 4) << 3) + (lane & 7);
-      const int chunk = kk * 2 + ((lane >> 3) & 1);
-      uint32_t b[4];
-      ldsm4(b, ks + swz(row, chunk));
-      mma_bf16(s[2 * np], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[0], b[1]);
-      mma_bf16(s[2 * np + 1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b[2], b[3]);
-    }
-  }
-  // scale to log2 units in fp32 (q stays exactly the stored bf16), mask,
-  // online softmax
-  const int t = lane & 3;
-  float mx0 = F.m[0], mx1 = F.m[1];
-#pragma unroll
-  for (int n = 0; n < 8; ++n) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) s[n][e] *= kScaleLog2;
-    const int p0 = tile_pos0 + n * 8 + 2 * t;
-    if (CAUSAL) {
-      if (p0 > lim0) s[n][0] = -INFINITY;
-      if (p0 + 1 > lim0) s[n][1] = -INFINITY;
-      if (p0 > lim1) s[n][2] = -INFINITY;
-      if (p0 + 1 > lim1) s[n][3] = -INFINITY;
-    }
-    mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
-    mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
-  }
-  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-  const float base0 = mx0 == -INFINITY ? 0.f : mx0;
-  const float base1 = mx1 == -INFINITY ? 0.f : mx1;
-  const float c0 = exp2f(F.m[0] - base0), c1 = exp2f(F.m[1] - base1);
-  F.m[0] = mx0;
-  F.m[1] = mx1;
-  float rs0 = 0.f, rs1 = 0.f;
-  // P as bf16 A fragments for 4 position k-steps of 16, split hi + lo so the
-  // P V product keeps ~16 mantissa bits of P (the oracle keeps P in fp32)
-  uint32_t pa[4][4], pl[4][4];
-#pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    const float e0 = exp2f(s[n][0] - base0), e1 = exp2f(s[n][1] - base0);
-    const float e2 = exp2f(s[n][2] - base1), e3 = exp2f(s[n][3] - base1);
-    rs0 += e0 + e1;
-    rs1 += e2 + e3;
-    const uint32_t h01 = f2_to_bf2(e0, e1), h23 = f2_to_bf2(e2, e3);
-    const float2 r01 = bf2_to_f2(h01), r23 = bf2_to_f2(h23);
-    const uint32_t l01 = f2_to_bf2(e0 - r01.x, e1 - r01.y), l23 = f2_to_bf2(e2 - r23.x, e3 - r23.y);
-    const int kk = n >> 1, o = (n & 1) * 2;
-    pa[kk][o] = h01;
-    pa[kk][o + 1] = h23;
-    pl[kk][o] = l01;
-    pl[kk][o + 1] = l23;
-  }
-  F.l[0] = F.l[0] * c0 + rs0;
-  F.l[1] = F.l[1] * c1 + rs1;
-#pragma unroll
-  for (int d = 0; d < 16; ++d) {
-    F.o[d][0] *= c0; F.o[d][1] *= c0;
-    F.o[d][2] *= c1; F.o[d][3] *= c1;
-  }
-  // O += P V : k = positions (4 steps of 16), n = dims (16 tiles of 8)
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk) {
-#pragma unroll
-    for (int dp = 0; dp < 8; ++dp) {  // pairs of dim n-tiles
-      // trans x4: (pos kk*16+0..7, dims dp*16+0..7), (pos +8..15, same dims),
-      //           (pos +0..7, dims +8..15), (pos +8..15, dims +8..15)
-      const int row = kk * 16 + (((lane >> 3) & 1) << 3) + (lane & 7);
-      const int chunk = dp * 2 + (lane >> 4);
-      uint32_t b[4];
-      ldsm4t(b, vs + swz(row, chunk));
-      mma_bf16(F.o[2 * dp], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b[0], b[1]);
-      mma_bf16(F.o[2 * dp + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b[2], b[3]);
-      if (PLO) {
-        mma_bf16(F.o[2 * dp], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b[0], b[1]);
-        mma_bf16(F.o[2 * dp + 1], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b[2], b[3]);
-      }
-    }
-  }
-}
-
 // Query row -> (token, head) inside one kv head's group
 SR_DEV const __nv_bfloat16* q_row_ptr(const AttnParams& p, int G, int g, int r) {
   const int tok = r / G, j = r % G;
   return p.q + (size_t)tok * p.n_heads * kHeadDim + (size_t)(g * G + j) * kHeadDim;
-}
-
-__global__ void __launch_bounds__(kTcaThreads) attn_prefill_tc_kernel(AttnParams p, int M_rows, int G) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  TcaSmem& sm = *reinterpret_cast<TcaSmem*>(smem_raw);
-
-  grid_launch_dependents();
-  grid_wait();
-
-  const int g = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int* ptab = p.page_table;
-  const int start = p.start_pos;  // position of token 0
-  const int row0 = qt * kRowsPerCta;
-  const int rows_here = min(kRowsPerCta, M_rows - row0);
-  constexpr bool warp_split_kv = false;  // (decode has its own cluster kernel)
-
-  // KV extent of this query tile: positions <= start + last token of the tile
-  const int last_tok = (row0 + rows_here - 1) / G;
-  const int T = start + last_tok + 1;
-  const int n_tiles = (T + kTile - 1) / kTile;
-  const int nsplit = gridDim.y;
-  const int per = (n_tiles + nsplit - 1) / nsplit;
-  const int t_lo = split * per;
-  const int t_hi = min(n_tiles, t_lo + per);
-
-  // ---- Q tile -> smem (bf16 as stored), swizzled rows ----
-  const uint32_t qs = s_u32(sm.q);
-  for (int i = tid; i < kRowsPerCta * 16; i += kTcaThreads) {
-    const int r = i >> 4, c = i & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < rows_here) {
-      v = reinterpret_cast<const uint4*>(q_row_ptr(p, G, g, row0 + r))[c];
-    }
-    *reinterpret_cast<uint4*>(sm.q + swz(r, c)) = v;
-  }
-
-  // ---- KV tile loader (one page: 64 rows x 256 B for K and for V) ----
-  auto load_tile = [&](int tile, int buf) {
-    const int page = ptab[tile];
-    const size_t off = kv_offset(p.layer, page, g, 0, p.n_pages, p.n_kv);
-    const uint8_t* kg = reinterpret_cast<const uint8_t*>(p.k_pool + off);
-    const uint8_t* vg = reinterpret_cast<const uint8_t*>(p.v_pool + off);
-    const uint32_t kb = s_u32(sm.k[buf]), vb = s_u32(sm.v[buf]);
-    for (int i = tid; i < kTile * 16; i += kTcaThreads) {
-      const int r = i >> 4, c = i & 15;
-      cpa16(kb + swz(r, c), kg + r * 256 + c * 16);
-      cpa16(vb + swz(r, c), vg + r * 256 + c * 16);
-    }
-  };
-
-  // which tiles this warp consumes, and which query rows it owns
-  const int my_rows0 = warp * 16;
-  Flash F;
-#pragma unroll
-  for (int d = 0; d < 16; ++d) F.o[d][0] = F.o[d][1] = F.o[d][2] = F.o[d][3] = 0.f;
-  F.m[0] = F.m[1] = -INFINITY;
-  F.l[0] = F.l[1] = 0.f;
-  const int gq = lane >> 2;
-  const int r_a = row0 + my_rows0 + gq, r_b = r_a + 8;
-  const int lim_a = start + (r_a < M_rows ? r_a : M_rows - 1) / G;
-  const int lim_b = start + (r_b < M_rows ? r_b : M_rows - 1) / G;
-
-  if (t_lo < t_hi) load_tile(t_lo, 0);
-  cpa_commit();
-  __syncthreads();  // Q tile visible
-
-  uint32_t qa[8][4];
-  const bool warp_active = my_rows0 < rows_here;
-  if (warp_active) {
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int row = my_rows0 + (lane & 15);
-      const int chunk = kk * 2 + (lane >> 4);
-      ldsm4(qa[kk], qs + swz(row, chunk));
-    }
-  }
-
-  for (int tile = t_lo; tile < t_hi; ++tile) {
-    const int buf = (tile - t_lo) & 1;
-    if (tile + 1 < t_hi) load_tile(tile + 1, buf ^ 1);
-    cpa_commit();
-    cpa_wait<1>();
-    __syncthreads();
-    if (warp_active) {
-      const int pos0 = tile * kTile;
-      // warp-uniform (the tile functions are full of .sync.aligned ops): mask
-      // whenever the tile reaches past the warp's *first* row's limit
-      const int warp_lim = start + (row0 + my_rows0) / G;
-      const bool need_mask = pos0 + kTile - 1 > warp_lim;
-      const uint32_t ks = s_u32(sm.k[buf]), vs = s_u32(sm.v[buf]);
-      if (p.p_hi_only) {  // P as plain bf16 (one P.V product)
-        if (need_mask) flash_tile<true, false>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
-        else flash_tile<false, false>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
-      } else {
-        if (need_mask) flash_tile<true>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
-        else flash_tile<false>(F, qa, ks, vs, lane, pos0, lim_a, lim_b);
-      }
-    }
-    __syncthreads();
-  }
-  cpa_wait<0>();
-
-  // ---- finalise row sums within the quad ----
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    F.l[i] += __shfl_xor_sync(0xffffffffu, F.l[i], 1);
-    F.l[i] += __shfl_xor_sync(0xffffffffu, F.l[i], 2);
-  }
-
-  const size_t part_stride = kHeadDim + 2;
-  {
-    // prefill: each warp writes its own 16 rows straight from registers
-    if (warp_active) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int rr = my_rows0 + gq + 8 * h;
-        if (rr >= rows_here) continue;
-        const int r = row0 + rr;
-        const float Lx = F.l[h], Mx = F.m[h];
-        if (nsplit == 1) {
-          __nv_bfloat16* o = const_cast<__nv_bfloat16*>(q_row_ptr(p, G, g, r)) - p.q + p.out;
-          const float inv = Lx > 0.f ? 1.f / Lx : 0.f;
-          for (int d = 0; d < 16; ++d) {
-            const int col = d * 8 + 2 * (lane & 3);
-            *reinterpret_cast<uint32_t*>(o + col) = f2_to_bf2(F.o[d][2 * h] * inv, F.o[d][2 * h + 1] * inv);
-          }
-        } else {
-          float* part = p.part + ((size_t)r * nsplit + split) * part_stride + (size_t)g * M_rows * nsplit * part_stride;
-          for (int d = 0; d < 16; ++d) {
-            const int col = d * 8 + 2 * (lane & 3);
-            part[col] = F.o[d][2 * h];
-            part[col + 1] = F.o[d][2 * h + 1];
-          }
-          if ((lane & 3) == 0) { part[kHeadDim] = Mx; part[kHeadDim + 1] = Lx; }
-        }
-      }
-    }
-  }
-  // split partials are merged by attn_merge_kernel (grid-wide, fixed split order)
 }
 
 // Split merge for prefill as its own grid-wide kernel: thread = (query row,
@@ -630,38 +382,10 @@ cudaError_t attn_decode_tc_launch(const AttnParams& p, cudaStream_t stream, bool
   return cudaLaunchKernelEx(&cfg, attn_decode_tc_kernel, p, G);
 }
 
-int attn_tc_splits(int n_kv, int q_tiles, int T, int num_sms) {
-  const int tiles = (T + kTile - 1) / kTile;
-  int s = 2 * num_sms / (n_kv * q_tiles);  // two CTAs per SM (81 KB smem each)
-  if (s > tiles) s = tiles;
-  if (s > kAttnMaxSplit) s = kAttnMaxSplit;
-  return s < 1 ? 1 : s;
-}
-
-cudaError_t attn_tc_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream,
-                           bool pdl) {
-  const int G = p.n_heads / p.n_kv;
-  const int M_rows = M_tokens * G;
-  const int q_tiles = (M_rows + kRowsPerCta - 1) / kRowsPerCta;
-  if (nsplit > kAttnMaxSplit) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(TcaSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_kv, nsplit, q_tiles);
-  cfg.blockDim = dim3(kTcaThreads);
-  cfg.dynamicSmemBytes = sizeof(TcaSmem);
-  cfg.stream = stream;
-  cudaLaunchAttribute attr_l[1];
-  attr_l[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr_l[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  cfg.attrs = attr_l;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, attn_prefill_tc_kernel, p, M_rows, G);
+// decode attention splits per kv head: ~one CTA per SM at long contexts
+int attn_decode_splits(int n_kv, int num_sms) {
+  int s = (num_sms + n_kv - 1) / n_kv;
+  return s < 1 ? 1 : (s > kAttnMaxSplit ? kAttnMaxSplit : s);
 }
 
 }  // namespace sr

@@ -91,7 +91,6 @@ struct AttnParams {
   unsigned int* counters;    // [M, KV]
   int layer, n_pages, n_heads, n_kv, nsplit;
   int start_pos;             // prefill: position of row 0
-  int p_hi_only;             // prefill: P.V with bf16 P only (no hi/lo split)
   DecodeState* st;           // decode: ctx_len / page table from here
   // multi-sequence prefill (umma kernel): per grid-z item (first token, tokens,
   // start position, query tile of the span) and that span's page table
@@ -99,16 +98,10 @@ struct AttnParams {
   const int* const* span_tables;
 };
 
-cudaError_t attn_decode_launch(const AttnParams& p, cudaStream_t stream, bool pdl);
 int attn_decode_splits(int n_kv, int num_sms);
-int attn_prefill_splits(int T);
 // tensor-core flash attention (attention_tc.cu)
 cudaError_t attn_decode_tc_launch(const AttnParams& p, cudaStream_t stream, bool pdl);
-cudaError_t attn_tc_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream,
-                           bool pdl);
-int attn_tc_splits(int n_kv, int q_tiles, int T, int num_sms);
 cudaError_t attn_merge_launch(const AttnParams& p, int M_tokens, int nsplit, cudaStream_t stream);
-cudaError_t attn_prefill_launch(const AttnParams& p, int M, cudaStream_t stream);
 // tcgen05 flash attention (attention_umma.cu); tmK / tmV: 128-B swizzled tensor
 // maps over the K / V pools viewed as [rows = L*n_pages*n_kv*64, 128], box 64x64
 cudaError_t attn_umma_launch(const void* tmK, const void* tmV, const AttnParams& p, int M_tokens,
@@ -117,15 +110,6 @@ int attn_umma_splits(int n_kv, int q_tiles, int T, int num_sms);
 int attn_umma_q_tiles(int M_tokens, int G);
 
 // ----------------------------------------------------------- prefill path ---
-// C_partial[s][m][n] = sum_{k in split s} A[m][k] * B[n][k]
-struct GemmParams {
-  const __nv_bfloat16* A;  // [M, K]
-  const __nv_bfloat16* B;  // [N, K]
-  float* C;                // [splits, M, N]
-  int M, N, K, splits;
-};
-cudaError_t gemm_launch(const GemmParams& p, cudaStream_t stream);
-int gemm_pick_splits(int M, int N, int K, int num_sms);
 
 // tcgen05 / TMEM / TMA version (gemm_tc.cu); tensor maps are CUtensorMap
 // (128 B, 64-B aligned) built by make_tmap_bf16

@@ -7,147 +7,6 @@
 
 namespace sr {
 
-// ============================================================== GEMM (v1) ==
-// C[s][m][n] = sum_k A[m][k] * B[n][k] over split s's K range.
-// Tile 64 (tokens) x 128 (weight rows) x 32, 8 warps (2 x 4), warp tile 32x32,
-// mma.sync m16n8k16 bf16 -> fp32, 3-stage cp.async ring, ldmatrix fragments.
-constexpr int BM = 64, BN = 128, BK = 32, STAGES = 3;
-constexpr int LDS = BK + 8;  // padded row (80 B): conflict-free ldmatrix
-
-SR_DEV void cp_async16(void* smem, const void* gmem, bool pred) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n));
-}
-SR_DEV void cp_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-SR_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
-
-SR_DEV void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(p);
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(s));
-}
-
-SR_DEV void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__global__ void __launch_bounds__(256) gemm_mma_kernel(GemmParams p) {
-  __shared__ __align__(16) __nv_bfloat16 As[STAGES][BM][LDS];
-  __shared__ __align__(16) __nv_bfloat16 Bs[STAGES][BN][LDS];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, split = blockIdx.z;
-  const int k_per = ((p.K / BK + p.splits - 1) / p.splits) * BK;
-  const int kbeg = split * k_per;
-  const int kend = min(p.K, kbeg + k_per);
-  const int nk = kend > kbeg ? (kend - kbeg) / BK : 0;
-
-  auto load_stage = [&](int st, int kt) {
-    const int k0 = kbeg + kt * BK;
-    // A: 64 rows x 32 cols = 256 x 16B chunks (one per thread)
-    {
-      const int r = tid >> 2, c = (tid & 3) * 8;
-      const int gm = m0 + r;
-      const bool ok = gm < p.M;
-      cp_async16(&As[st][r][c], p.A + (size_t)(ok ? gm : 0) * p.K + k0 + c, ok);
-    }
-    // B: 128 rows x 32 cols = 512 chunks (two per thread)
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int idx = tid + i * 256;
-      const int r = idx >> 2, c = (idx & 3) * 8;
-      const int gn = n0 + r;
-      const bool ok = gn < p.N;
-      cp_async16(&Bs[st][r][c], p.B + (size_t)(ok ? gn : 0) * p.K + k0 + c, ok);
-    }
-  };
-
-  float acc[2][4][4];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.f;
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage(s, s);
-    cp_commit();
-  }
-  for (int kt = 0; kt < nk; ++kt) {
-    cp_wait<STAGES - 2>();
-    __syncthreads();
-    const int nxt = kt + STAGES - 1;
-    if (nxt < nk) load_stage(nxt % STAGES, nxt);
-    cp_commit();
-    const int st = kt % STAGES;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 16) {
-      uint32_t a[2][4];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int r = wm * 32 + i * 16 + (lane & 15);
-        const int c = kk + (lane >> 4) * 8;
-        ldsm_x4(a[i][0], a[i][1], a[i][2], a[i][3], &As[st][r][c]);
-      }
-      uint32_t b[4][2];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {  // two x4 loads = four n8 tiles
-        const int r = wn * 32 + j * 16 + (lane >> 4) * 8 + (lane & 7);
-        const int c = kk + ((lane >> 3) & 1) * 8;
-        uint32_t r0, r1, r2, r3;
-        ldsm_x4(r0, r1, r2, r3, &Bs[st][r][c]);
-        b[2 * j][0] = r0; b[2 * j][1] = r1; b[2 * j + 1][0] = r2; b[2 * j + 1][1] = r3;
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) mma16816(acc[i][j], a[i], b[j][0], b[j][1]);
-    }
-  }
-  cp_wait<0>();
-
-  float* C = p.C + (size_t)split * p.M * p.N;
-  const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int col = n0 + wn * 32 + j * 8 + 2 * t;
-#pragma unroll
-      for (int hrow = 0; hrow < 2; ++hrow) {
-        const int row = m0 + wm * 32 + i * 16 + g + hrow * 8;
-        if (row < p.M && col < p.N) {
-          float2 v = make_float2(acc[i][j][2 * hrow], acc[i][j][2 * hrow + 1]);
-          if (col + 1 < p.N) *reinterpret_cast<float2*>(C + (size_t)row * p.N + col) = v;
-          else C[(size_t)row * p.N + col] = v.x;
-        }
-      }
-    }
-}
-
-int gemm_pick_splits(int M, int N, int K, int num_sms) {
-  const int tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
-  int s = 1;
-  while (tiles * s < num_sms && (K / BK) / (s * 2) >= 8 && s < 16) s *= 2;
-  return s;
-}
-
-cudaError_t gemm_launch(const GemmParams& p, cudaStream_t stream) {
-  if (p.K % BK != 0) return cudaErrorInvalidValue;
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.splits);
-  gemm_mma_kernel<<<grid, 256, 0, stream>>>(p);
-  return cudaGetLastError();
-}
-
 // ========================================================= epilogues ======
 constexpr int kEpiThreads = 256;
 constexpr int kEpiRowThreads = 1024;  // one CTA per token row: wide, for latency

@@ -141,7 +141,6 @@ struct Model {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   sr_timing timing{};
   bool pdl = true;
-  bool use_tc = true;  // tcgen05 GEMM (K6); SR_GEMM=mma selects the mma.sync reference
   bool stream_decode = false;  // SR_DECODE=stream: per-token host loop (profiling only)
   bool graph_decode = false;   // SR_DECODE=graph: per-kernel decode graph (A/B reference)
   MkParams mk{};
@@ -152,8 +151,6 @@ struct Model {
   float* tp_delta = nullptr;
   float *tp_send, *tp_gather, *tp_dig, *tp_dec;
   int* tp_counts;
-  bool attn_simt = false;      // SR_ATTN=simt: CUDA-core split-KV attention (A/B reference)
-  bool attn_umma = true;       // tcgen05 prefill attention; SR_ATTN=tc: mma.sync (A/B)
   bool prefetch = false;       // SR_PREFETCH=1: GEMV L2 prefetch before the PDL wait
   bool feed1 = true;           // one fed token decodes in the persistent kernel (SR_FEED1=0: prefill)
   struct alignas(64) TMap { CUtensorMap m; };
@@ -365,7 +362,7 @@ struct Model {
       a.n_kv = d.n_kv_heads;
       a.nsplit = L.nsplit_decode;
       a.st = st;
-      e = attn_simt ? attn_decode_launch(a, s, pdl) : attn_decode_tc_launch(a, s, pdl);
+      e = attn_decode_tc_launch(a, s, pdl);
       if (e != cudaSuccess) return e;
 
       p = gemv_base();
@@ -474,7 +471,7 @@ struct Model {
     SR_CK(embed_norm_launch(ids, M, embed, d.d_model, lw(0, LN1), d.rms_eps, h, x, s));
     // several spans on the tcgen05 attention: one launch per layer over a
     // (span, query tile) item table
-    const bool multi = n_spans > 1 && attn_umma && !attn_simt;
+    const bool multi = n_spans > 1;
     int n_items = 0, t_max = 0;
     if (multi) {
       const int G = d.n_heads / d.n_kv_heads;
@@ -546,10 +543,7 @@ struct Model {
         const int Tlast = sp.start + sp.M;
         a.start_pos = sp.start;
         a.st = nullptr;
-        if (attn_simt) {
-          a.nsplit = std::min(kAttnPrefillSplit, attn_prefill_splits(Tlast));
-          SR_CK(attn_prefill_launch(a, sp.M, s));
-        } else if (attn_umma) {
+        {
           const int G = d.n_heads / d.n_kv_heads;
           a.nsplit = std::min(kAttnPrefillSplit, attn_umma_splits(d.n_kv_heads,
                                                                   attn_umma_q_tiles(sp.M, G),
@@ -557,14 +551,6 @@ struct Model {
           SR_CK(attn_umma_launch(&kvmaps[0].m, &kvmaps[1].m, a, sp.M, a.nsplit, s));
           if (a.nsplit > 1) SR_CK(attn_merge_launch(a, sp.M, a.nsplit, s));
           watch(s, "attn_prefill_umma", l, sp.M, a.nsplit);
-        } else {
-          const int G = d.n_heads / d.n_kv_heads;
-          const int q_tiles = (sp.M * G + 63) / 64;
-          a.nsplit = std::min(kAttnPrefillSplit, attn_tc_splits(d.n_kv_heads, q_tiles, Tlast, num_sms));
-          a.p_hi_only = p_hi_only ? 1 : 0;
-          SR_CK(attn_tc_launch(a, sp.M, a.nsplit, s, true));
-          if (a.nsplit > 1) SR_CK(attn_merge_launch(a, sp.M, a.nsplit, s));
-          watch(s, "attn_prefill_tc", l, sp.M, a.nsplit);
         }
       }
       // o-proj + residual + norm2
@@ -716,7 +702,6 @@ struct Model {
   // SR_ATTN_PHI=1: prefill attention with bf16 P only.  Off: the hi/lo split
   // of P is needed for the tiny-model parity bound (measured: bf16 P fails
   // tests/test_gpu_parity.py) and costs only ~2-3 % of a verify pass
-  bool p_hi_only = false;
   // SR_WATCH=1: synchronise after each prefill stage and abort with the stage
   // name if it does not finish within 10 s (bring-up aid for device hangs)
   bool watch_on = false;
@@ -741,7 +726,7 @@ struct Model {
   int gemm(int act_id, int wmap, const __nv_bfloat16* A, const __nv_bfloat16* B, int M, int N,
            int K, cudaStream_t s, __nv_bfloat16* glu_out = nullptr) {
     fused_glu = false;
-    if (use_tc) {
+    {
       TcGemmArgs a{};
       a.act = glu_out;
       const int nt = tc_pick_tile(M, N, num_sms);
@@ -761,20 +746,6 @@ struct Model {
       SR_CK(gemm_tc_launch(a, s));
       return 0;
     }
-    GemmParams g{};
-    g.A = A;
-    g.B = B;
-    g.C = part;
-    g.M = M;
-    g.N = N;
-    g.K = K;
-    int sp = gemm_pick_splits(M, N, K, num_sms);
-    while (sp > 1 && (size_t)sp * M * N > L.part_floats) sp /= 2;
-    sp = std::min(sp, kPrefillSplitsMax);
-    g.splits = sp;
-    last_splits = sp;
-    SR_CK(gemm_launch(g, s));
-    return 0;
   }
 
   EpiParams epi_base(int M, int N) const {
@@ -888,18 +859,12 @@ int sr_model_create(const sr_model_desc* desc, const sr_model_ptrs* ptrs, void* 
   }
   for (auto& ev : m->ev) cudaEventCreate(&ev);
   if (const char* v = getenv("SR_NO_PDL")) m->pdl = (v[0] == '0');
-  if (const char* v = getenv("SR_GEMM")) m->use_tc = strcmp(v, "mma") != 0;
   if (const char* v = getenv("SR_DECODE")) {
     m->stream_decode = strcmp(v, "stream") == 0;
     m->graph_decode = strcmp(v, "graph") == 0;
   }
-  if (const char* v = getenv("SR_ATTN")) {
-    m->attn_simt = strcmp(v, "simt") == 0;
-    m->attn_umma = strcmp(v, "tc") != 0 && !m->attn_simt;
-  }
   if (const char* v = getenv("SR_PREFETCH")) m->prefetch = v[0] == '1';
   if (const char* v = getenv("SR_FEED1")) m->feed1 = v[0] != '0';
-  if (const char* v = getenv("SR_ATTN_PHI")) m->p_hi_only = v[0] == '1';
   if (const char* v = getenv("SR_WATCH")) {
     m->watch_on = atoi(v) > 0;
     m->watch_ms = atoi(v) > 1 ? atoi(v) * 1000 : 10000;
