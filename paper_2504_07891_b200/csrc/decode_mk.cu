@@ -1350,9 +1350,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
   while (!done) {
     MK_EV();
     const int npages = pos / kPage + 1;
-    // splits per kv head: every CTA busy at long context, >= 2 pages per split
-    int S_a = G / p.KV;
-    if (S_a > (npages + p.min_pages - 1) / p.min_pages) S_a = (npages + p.min_pages - 1) / p.min_pages;
+    // splits per kv head: the fewest that keep the largest split at the page
+    // count the CTAs allow (96 pages over 74 CTAs would hold 1 or 2 pages
+    // each; 48 splits of 2 pages finish at the same time with less COMBINE
+    // work: 1.5B at 6 K 1.153 -> 1.123 ms/token)
+    const int smax = G / p.KV;
+    int per = (npages + smax - 1) / smax;
+    if (per < p.min_pages) per = p.min_pages;
+    int S_a = (npages + per - 1) / per;
+    if (S_a > smax) S_a = smax;
     if (S_a < 1) S_a = 1;
     // more CTAs than page splits (short contexts): split each page's query
     // heads over hs CTAs too, so idle CTAs share the per-page latency chain

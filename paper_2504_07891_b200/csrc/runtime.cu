@@ -294,7 +294,7 @@ struct Model {
     // slower on B200 (the extra HBM traffic delays the latency-bound phases)
     p.l2_ahead = -1;
     if (const char* v = getenv("SR_MK_L2AHEAD")) p.l2_ahead = atoi(v);
-    p.head_split = 1;
+    p.head_split = 0;  // SR_MK_HEADSPLIT=1: split a page's heads over idle CTAs (round 1; no gain with the tensor-core attention)
     if (const char* v = getenv("SR_MK_HEADSPLIT")) p.head_split = atoi(v);
     p.bar_sleep = 0;
     p.evict_first = 1;
