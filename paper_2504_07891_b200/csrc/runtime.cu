@@ -930,8 +930,8 @@ int sr_generate(void* model, const int32_t* page_table, int32_t start_pos, const
     SR_CK(cudaEventRecord(m->ev[1], s));
     SR_CK(mk_launch(m->mk, m->L.mk_g, s));
     SR_CK(cudaEventRecord(m->ev[2], s));
-    m->timing.prefill_tokens = 0;
-    m->timing.decode_tokens = 0;  // filled from the output header by the caller
+    m->timing.prefill_tokens = 0;  // tells the caller every new token was a decode step
+    m->timing.decode_tokens = -1;  // filled by the caller from out[0]
     return 0;
   }
   SR_CK(decode_begin_launch(m->st, &init, s));
