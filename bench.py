@@ -268,6 +268,8 @@ def call_descriptors(backend, calls, model_key: str) -> list[dict]:
                      finish=fin)
         else:
             d.update(score=c["score"], n_gen=1)
+            if c.get("catchup"):  # generation-stream rows prefilled in the same pass
+                d.update(catchup=c["catchup"], catchup_start=c["catchup_start"])
         out.append(d)
     return out
 

@@ -193,6 +193,9 @@ class CpuReplay:
         t0 = time.perf_counter()
         if call["kind"] == "score":
             t = m.score(call["start"], call["fresh"], layers=lay)
+            if call.get("catchup"):  # the generation stream's rows of the same pass,
+                # which the reference's own fallback call would prefill instead
+                t += m.generate(call["catchup_start"], call["catchup"], 0, layers=lay)
         else:
             t = m.generate(call["start"], call["fresh"], call["n_gen"], layers=lay,
                            decode_cap=self.decode_cap)

@@ -249,6 +249,10 @@ class _Pages:
 class NativeEngine:
     """``host.DeviceEngine`` over a ``DeviceModel``."""
 
+    # several streams' fresh rows share one device pass (sr_score_batch): a
+    # scoring call extends the generation stream in the same pass
+    multi_span_passes = True
+
     def __init__(self, model: DeviceModel, vocab: Vocab) -> None:
         self.model = model
         self.spec = model.spec

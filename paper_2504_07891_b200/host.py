@@ -33,6 +33,7 @@ only the rest -- the commit.
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -214,6 +215,11 @@ class ModelBackend(Backend):
         self.record = record
         self.calls: list[dict] = []   # per-call trace (ids) for replay parity
         self.verify_template = "v1"   # "v2": prefix-sharing verification prompts
+        # a scoring call also prefills the base's generation stream up to the
+        # same CoT (all but its last prompt token) in the same device pass, so
+        # a fallback or the next base generation feeds one token and starts in
+        # the decode kernel instead of a prefill pass (SR_CATCHUP=0: off)
+        self.catch_up = os.environ.get("SR_CATCHUP", "1") != "0"
 
     # -- token-level speculation (SpecReason+Decode) ----------
     def attach_speculator(self, draft: "ModelBackend", gamma: int = 5) -> None:
@@ -455,6 +461,29 @@ class ModelBackend(Backend):
         return T.GenerationResult(text=text, token_count=len(text_ids), finish_reason=reason,
                                   measured_latency_s=time.monotonic() - t0)
 
+    def _catch_up_plan(self, request, vstream, v_rows: int):
+        """(stream, keep, ids) of the generation stream a scoring call extends
+        in its own device pass, or None.  The generation prompt of the same CoT
+        (``render_generation_prompt(problem, cot_prefix)``: what a fallback or
+        the next base generation feeds) is cached up to its last token, on the
+        stream with the longest common prefix other than the verify stream.
+        Only when at least two rows are missing: with one, the generation
+        already starts in the decode kernel (``sr_generate``'s one-token path),
+        which keeps a base that generates every step (threshold 10) computing
+        exactly what ``run_vanilla`` does."""
+        if (not self.catch_up or self.verify_template != "v1" or len(self.pool.streams) < 2
+                or not getattr(self.engine, "multi_span_passes", False)):
+            return None
+        gids = self._prompts.encode(domain.render_generation_prompt(request.problem,
+                                                                    request.cot_prefix))
+        if len(gids) < 3:
+            return None
+        gst, gkeep = self.pool.acquire(gids[:-1], exclude=(vstream,))
+        n = len(gids) - 1 - gkeep
+        if n < 2 or n + v_rows > self.engine.model.max_tokens:
+            return None
+        return gst, gkeep, gids
+
     def _score_step(self, request: VerificationRequest):
         T = self.types
         if self.profile.role != T.BackendRole.BASE:
@@ -469,12 +498,21 @@ class ModelBackend(Backend):
             ids = self._prompts.encode(prompt)
             stream, keep = self.pool.acquire(ids)
             self.engine.truncate(stream, keep)
-            r = self.engine.score(stream, ids[keep:], self.threshold)
+            catch = self._catch_up_plan(request, stream, len(ids) - keep)
+            if catch is None:
+                r = self.engine.score(stream, ids[keep:], self.threshold)
+            else:
+                gst, gkeep, gids = catch
+                self.engine.truncate(gst, gkeep)
+                r = self.engine.score_batch([stream, gst], [ids[keep:], gids[gkeep:-1]],
+                                            self.threshold)[0]
             if self.record:
                 self.calls.append({"kind": "score", "prompt_ids": ids, "score": r.score,
                                    "accept": r.accept, "margin": r.margin,
                                    "argmax": r.argmax, "fresh": len(ids) - keep,
-                                   "seq": time.monotonic_ns()})
+                                   "seq": time.monotonic_ns(),
+                                   **({"catchup_start": catch[1],
+                                       "catchup": len(catch[2]) - 1 - catch[1]} if catch else {})})
         if r.score < 0:
             raise T.ScoreParseFailure("no digit in the top-10 or the sampled token")
         return T.UtilityScore(r.score)
