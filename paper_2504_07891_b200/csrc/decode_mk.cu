@@ -7,11 +7,13 @@
 //   * a producer warp: one lane streams the CTA's share of every weight matrix
 //     of the model -- layer 0 qkv, o, gate/up, down, layer 1 ..., LM head, then
 //     the next token's layer 0 ... -- as 32-row x 256-column bf16 tiles (16 KB)
-//     through a TMA (cp.async.bulk.tensor) + mbarrier ring of up to 13 stages
-//     (~200 KB in flight per SM).  Weights are constant, so the producer never
-//     waits for activations: it runs ahead across phase and grid barriers and
-//     even into the next token, bounded only by the ring.  HBM streaming
-//     therefore does not stop while the consumers synchronise;
+//     into an mbarrier ring of up to 13 stages (2 tiles each).  Default
+//     (kTiled): from the tile-major, pre-swizzled copy of the weights
+//     (sr_model_set_decode_tiles), one contiguous 16 KB cp.async.bulk per
+//     tile; else (SR_MK_TILED=0) a TMA box of the row-major weights.  Weights
+//     are constant, so the producer never waits for activations: it runs
+//     ahead across phase and grid barriers and into the next token, bounded
+//     only by the ring;
 //   * 16 consumer warps that run the token's phases in order, separated by
 //     grid barriers (one atomic counter, acquire/release):
 //
@@ -19,30 +21,33 @@
 //
 // GEMV phases.  A phase's tiles ("units", row-block major, k minor) are cut
 // into G contiguous ranges, one per CTA, so every CTA streams the same number
-// of bytes (+-1 tile).  Warp w of a tile owns rows w and w+16 (lane = 8
-// columns, one 16-byte shared load per row); partial dot products stay in
-// registers across the k tiles of a row block and are reduced once per block
-// with warp shuffles.  A row block cut by a range boundary leaves one partial
-// per contributing CTA in `part[cta][j][32]`; the next phase's prologue sums
-// the 1-3 partials of each row in CTA order (deterministic, no atomics).
-// GATE/UP and LM head use block-granular ranges instead: the interleaved
-// gate/up layout (16 gate rows then the 16 matching up rows per 32-row block)
-// lets the gate/up epilogue emit silu(g)*u directly, and the LM head needs
-// whole logits for the greedy argmax.
+// of bytes (+-1 tile).  Tensor-core consumer (mk_gemv_mma, default): warp w
+// takes rows 16(w&1).. and columns 32(w>>1).. of every tile with two
+// mma.sync m16n8k16 (x as every column of B), accumulating over the k tiles
+// of a row block; at its end the 8 column slices of each row are summed in
+// fixed order through shared memory.  CUDA-core consumer (mk_gemv): warp w
+// owns rows w and w+16, lane = 8 columns.  A row block cut by a range
+// boundary leaves one partial per contributing CTA in `part[cta][j][32]`;
+// the next phase's prologue sums the partials of each row in CTA order
+// (deterministic, no atomics).  GATE/UP and LM head use block-granular ranges
+// instead: the interleaved gate/up layout (16 gate rows then the 16 matching
+// up rows per 32-row block) lets the gate/up epilogue emit silu(g)*u
+// directly, and the LM head needs whole logits for the greedy argmax.
 //
 // Prologues.  Every CTA rebuilds the GEMV input vector x in shared memory:
 // RMSNorm(h) from the fp32 residual stream plus the previous phase's partials
-// (CTA 0 writes the updated residual back; two buffers alternate so no CTA
-// reads a vector while it is rewritten), or a copy of the bf16 attention
-// output / activation.  All cross-CTA data is read with ld.global.cg (L2), never
-// through the non-coherent L1.
+// (16-B loads, one batch; CTA 0 writes the updated residual back; two buffers
+// alternate so no CTA reads a vector while it is rewritten), or a copy of the
+// bf16 attention output / activation.  All cross-CTA data is read with
+// ld.global.cg (L2), never through the non-coherent L1.
 //
 // Attention (K4).  CTA (kv head g, split s) takes a contiguous page range of
-// the paged K/V cache for the G = H/KV query heads of g: q and the new k/v are
-// summed from the qkv partials (+bias, RoPE, bf16 rounding as the oracle),
-// the CTA owning the last page appends k/v to the pool, scores use 8 lanes per
-// position (16 dims each), an exp2 online softmax per head, and P.V with one
-// thread per (dim, 16-position group).  COMBINE merges the split partials
+// the paged K/V cache for the query heads of g: q and the new k/v are summed
+// from the qkv partials (+bias, RoPE, bf16 rounding as the oracle), the CTA
+// owning the last page appends k/v to the pool.  Pages arrive as 128-B-
+// swizzled TMA boxes; S = Q.K^T and O += P.V run on mma.sync with an exp2
+// online softmax in between (P as bf16 hi + lo), pipelined over two warp
+// groups where a second page buffer fits.  COMBINE merges the split partials
 // per head into the bf16 attention output.
 //
 // LM head (K5).  Each CTA keeps a (top-1, index, top-2) over its rows; after
