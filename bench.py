@@ -8,11 +8,14 @@ thinking budget, 64-word synthetic problems (``dp.problem_text``).  One
 *step* is one iteration of the SpecReason thinking loop driven through the
 public API (``driver.SpecReasonSession`` over two ``B200Backend``s): the draft
 decodes a step, the base scores it in one prefill pass, and on reject the base
-regenerates it.  The timed window is mid-trajectory: an untimed fast-forward
-runs the trajectory to a quarter of its thinking budget (2048 CoT tokens),
-then W warm-up steps, then the K timed steps, which at ~25-90 tokens per step
-cover contexts of ~2.5-6 K (the 8 K trajectory's mean is 4 K) and stay inside
-the first trajectory (the reference arm replays that one trajectory).
+regenerates it.  The K timed steps are split over P = 4 windows
+(``--windows``), one per problem (task0000..), each mid-trajectory: an
+untimed fast-forward runs that problem's trajectory to a quarter of its
+thinking budget (2048 CoT tokens), then (first window only) W warm-up steps,
+then the window's share of the K timed steps, which at ~25-90 tokens per
+step cover contexts of ~2.5-6 K (an 8 K trajectory's mean is 4 K).  The loop
+metric follows the acceptance rate of the timed steps, so several problems'
+windows give a steadier number than one.
 
 Reported (one JSON line, rank 0):
   value      CoT tokens / s over the K timed steps, device time (sum of the
@@ -33,8 +36,8 @@ Multi-GPU (torchrun): ``--mode dp`` splits a fixed problem set by problem id
 (``dp.partition``; no collective on the data path, scaling "weak");
 ``--mode tp`` shards the base over the ranks (C4).
 ``--impl reference`` runs the unmodified reference engine (``baseline/_ref``)
-over a recorded C3 trajectory of this benchmark (``bench_data/``), pricing
-every warm-up and timed step's calls on the host cores (rank 0).
+over the recorded trajectories of this benchmark's windows (``bench_data/``),
+pricing every warm-up and timed step's calls on the host cores (rank 0).
 """
 
 from __future__ import annotations
@@ -306,7 +309,6 @@ def run_ours(args) -> None:
     ff = args.budget // 4 if args.ff_tokens < 0 else args.ff_tokens
     sched = None
     ff_steps = 0
-    warm_bounds: list = []
     if args.batch > 1:  # B trajectories, each on its own thread, batched device passes
         from paper_2504_07891_b200.batching import BatchScheduler
 
@@ -329,38 +331,75 @@ def run_ours(args) -> None:
         if ff > 0:
             sched.run([lambda s_, b_, src=src: src.fast_forward(ff) for src in srcs])
         run_steps(max(1, -(-args.warmup // args.batch)))
-    else:
-        src = StepSource(small, base, cfg, mine, vocab)
-        ff_steps = src.fast_forward(ff)
-        c_ff = (len(small.calls), len(base.calls))
-        for _ in range(args.warmup):
-            src.step()
-            warm_bounds.append((len(small.calls), len(base.calls)))
 
     stream = torch.cuda.current_stream()
-    s0 = (small.engine.stats.snapshot(), base.engine.stats.snapshot())
-    c0 = (len(small.calls), len(base.calls))
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    outcomes, bounds = [], []
+    outcomes: list = []
+    wins: list[dict] = []
     with ClockSampler(local) as clocks:
-        e0.record(stream)
         if sched is not None:
+            s0 = (small.engine.stats.snapshot(), base.engine.stats.snapshot())
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             outcomes = run_steps(per)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            wall_ms = e0.elapsed_time(e1)
+            ds = small.engine.stats.minus(s0[0])
+            db = base.engine.stats.minus(s0[1])
         else:
-            for _ in range(args.steps):
-                outcomes.append(src.step())
-                bounds.append((len(small.calls), len(base.calls)))
-        e1.record(stream)
-        torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    wall_ms = e0.elapsed_time(e1)
+            # the K timed steps are split over P windows, one per problem of
+            # this rank's block, each after its own untimed fast-forward (the
+            # W warm-up steps run before the first): the loop metric follows
+            # the acceptance rate of the window, so several trajectories'
+            # windows give a steadier number than one
+            from paper_2504_07891_b200.backend import EngineStats
+
+            P = max(1, min(args.windows, args.steps))
+            per_w = [args.steps // P + (1 if i < args.steps % P else 0) for i in range(P)]
+            wall_ms = 0.0
+            ds, db = EngineStats(), EngineStats()
+            for i, n in enumerate(per_w):
+                wsrc = StepSource(small, base, cfg, [mine[i % len(mine)]], vocab)
+                start = (len(small.calls), len(base.calls))
+                ff_i = wsrc.fast_forward(ff)
+                c_ff = (len(small.calls), len(base.calls))
+                warm = []
+                for _ in range(args.warmup if i == 0 else 0):
+                    wsrc.step()
+                    warm.append((len(small.calls), len(base.calls)))
+                s0 = (small.engine.stats.snapshot(), base.engine.stats.snapshot())
+                c0 = (len(small.calls), len(base.calls))
+                if dist is not None:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                outs, bounds = [], []
+                e0.record(stream)
+                for _ in range(n):
+                    outs.append(wsrc.step())
+                    bounds.append((len(small.calls), len(base.calls)))
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if dist is not None:
+                    dist.barrier()
+                wall_ms += e0.elapsed_time(e1)
+                ds = ds.plus(small.engine.stats.minus(s0[0]))
+                db = db.plus(base.engine.stats.minus(s0[1]))
+                outcomes += outs
+                ff_steps += ff_i
+                wins.append({"src": wsrc, "start": start, "ff_steps": ff_i, "c_ff": c_ff,
+                             "warm": warm, "c0": c0, "bounds": bounds, "outcomes": outs})
+
+            class _Wins:  # StepSource-like view for the shared reporting below
+                trajectories = sum(w["src"].trajectories for w in wins)
+
+            src = _Wins()
     n_steps = len(outcomes)  # --batch B runs ceil(steps / B) steps on each trajectory
-    ds = small.engine.stats.minus(s0[0])
-    db = base.engine.stats.minus(s0[1])
 
     tokens = sum(o.step.token_count for o in outcomes)
     dev_ms = ds.prefill_ms + ds.decode_ms + db.prefill_ms + db.decode_ms
@@ -426,13 +465,15 @@ def run_ours(args) -> None:
            if sched is not None else {}),
         "clocks": clocks.summary(),
     }
-    if record and args.dump_trace:
+    if record and args.dump_trace and wins:
         try:
-            dump_trace(args, src, small, base, ff_steps, c_ff, warm_bounds + bounds, names)
+            dump_trace(args, wins, small, base, names)
         except RuntimeError as exc:  # the line still prints; the trace is optional
             print(f"bench: no trace written: {exc}", file=sys.stderr, flush=True)
-    if world == 1 and not args.no_cpu_baseline and record:
-        result["cpu_baseline"] = cpu_baseline(args, small, base, names, c0, bounds, outcomes)
+    if world == 1 and not args.no_cpu_baseline and record and wins:
+        w0 = wins[0]
+        result["cpu_baseline"] = cpu_baseline(args, small, base, names, w0["c0"], w0["bounds"],
+                                              w0["outcomes"])
     print(json.dumps(result), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -477,9 +518,15 @@ def bench_config(args, world: int) -> dict:
             "pair": args.pair, "threshold": args.threshold, "verify_template": args.verify_template,
             "spec_gamma": args.spec_gamma, "token_budget": args.budget,
             "max_step_tokens": args.max_step_tokens, "batch": args.batch,
-            "timed_window": (f"after an untimed fast-forward to "
+            "timed_window": (f"the timed steps split over {max(1, min(args.windows, args.steps))} "
+                             f"windows on the first problems of the block, each after an untimed "
+                             f"fast-forward to "
                              f"{args.budget // 4 if args.ff_tokens < 0 else args.ff_tokens} CoT "
-                             f"tokens of the first problem, then the warm-up steps"),
+                             f"tokens (warm-up steps before the first)"
+                             if args.batch == 1 else
+                             f"after an untimed fast-forward of every trajectory to "
+                             f"{args.budget // 4 if args.ff_tokens < 0 else args.ff_tokens} CoT "
+                             f"tokens, then the warm-up steps"),
             "problems": f"task0000..task{args.problems - 1:04d} (dp.problem_text), split by id",
             "parallelism": (f"dp{world} (problem-id partition, no data-path collective"
                             + (f", {args.batch} concurrent trajectories per GPU sharing batched "
@@ -489,24 +536,31 @@ def bench_config(args, world: int) -> dict:
             "l2": "weights (3.5 + 65.5 GB) exceed L2 (126 MB) on every step: no flush needed"}
 
 
-def dump_trace(args, src, small, base, ff_steps, c_ff, step_ends, names) -> None:
-    """Write the first trajectory's calls up to the end of the timed window
-    (``--impl reference`` replays them through the reference engine): the
-    fast-forward's calls, then per warm-up / timed step the (small, base)
-    call counts at its end (``step_ends``)."""
-    if src.trajectories != 1:
-        raise RuntimeError("the trace covers one trajectory: raise --budget or lower --steps")
+def dump_trace(args, wins, small, base, names) -> None:
+    """Write every timed window's trajectory (``--impl reference`` replays
+    them through the reference engine): per window the problem, the calls of
+    its trajectory from its first call to the end of the window (fast-forward,
+    warm-up and timed steps), where the window starts and the (small, base)
+    call counts at the end of every warm-up / timed step -- all relative to
+    the window's first call."""
+    out = []
+    for w in wins:
+        if w["src"].trajectories != 1:
+            raise RuntimeError("a window ran past its trajectory: raise --budget or lower --steps")
+        s0 = w["start"]
+        ends = [(a - s0[0], b - s0[1]) for a, b in w["warm"] + w["bounds"]]
+        end = w["bounds"][-1]
+        out.append({"problem": w["src"].problems[0], "fast_forward_steps": w["ff_steps"],
+                    "warmup": len(w["warm"]), "steps": len(w["bounds"]),
+                    "window_start": [w["c_ff"][0] - s0[0], w["c_ff"][1] - s0[1]],
+                    "step_ends": [list(e) for e in ends],
+                    "small": call_descriptors(small, small.calls[s0[0]:end[0]], names[0]),
+                    "base": call_descriptors(base, base.calls[s0[1]:end[1]], names[1])})
     path = Path(args.dump_trace)
     path.parent.mkdir(parents=True, exist_ok=True)
-    end = step_ends[-1]
     path.write_text(json.dumps({
         "pair": args.pair, "budget": args.budget, "threshold": args.threshold,
-        "max_step_tokens": args.max_step_tokens, "problem": src.problems[0],
-        "fast_forward_steps": ff_steps, "window_start": list(c_ff),
-        "step_ends": [list(e) for e in step_ends],
-        "small": call_descriptors(small, small.calls[:end[0]], names[0]),
-        "base": call_descriptors(base, base.calls[:end[1]], names[1]),
-    }) + "\n")
+        "max_step_tokens": args.max_step_tokens, "windows": out}) + "\n")
 
 
 def cpu_baseline(args, small, base, names, c0, bounds, outcomes) -> dict:
@@ -615,8 +669,8 @@ def _replay_backend_cls(stepspec):
 
 def run_reference(args) -> None:
     """Reference arm: the unmodified reference engine (``run_trajectory``,
-    ``engine.py:297``) drives replay backends over this benchmark's recorded
-    C3 trajectory; every warm-up and timed step's calls are executed on the
+    ``engine.py:297``) drives replay backends over each recorded window's
+    trajectory of this benchmark; every warm-up and timed step's calls are executed on the
     host cores at full model shape, on a bounded per-call sample of layers and
     decode steps scaled back per call (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -638,10 +692,14 @@ def run_reference(args) -> None:
             print(json.dumps({"impl": "reference",
                               "unavailable": f"trace {k}={tr[k]} differs from --{k} {getattr(args, k)}"}))
             return
-    n_win = args.warmup + args.steps
-    if len(tr["step_ends"]) < n_win:
+    wins = tr["windows"]
+    P = max(1, min(args.windows, args.steps))
+    per_w = [args.steps // P + (1 if i < args.steps % P else 0) for i in range(P)]
+    warm_w = [args.warmup if i == 0 else 0 for i in range(P)]
+    if len(wins) < P or any(w["warmup"] + w["steps"] < a + n for w, a, n in zip(wins, warm_w, per_w)):
         print(json.dumps({"impl": "reference", "unavailable":
-                          f"trace window has {len(tr['step_ends'])} steps < warmup+steps {n_win}"}))
+                          f"trace holds {[w['warmup'] + w['steps'] for w in wins]} steps per window, "
+                          f"the run needs {[a + n for a, n in zip(warm_w, per_w)]}"}))
         return
     from oracle.cpu_replay import CpuReplay
     from paper_2504_07891_b200.shapes import PAIRS, get_spec
@@ -651,31 +709,35 @@ def run_reference(args) -> None:
     names = PAIRS[args.pair]
     t_start = time.perf_counter()
     # bounded sample per call (a layer sample and <= 16 decode steps, scaled
-    # back per call): the 45 steps' full-depth CPU work is tens of minutes
+    # back per call): the steps' full-depth CPU work is tens of minutes
     rep = CpuReplay({n: get_spec(n) for n in names}, max_ctx=args.budget + 1024,
                     layer_frac=args.ref_layer_frac, decode_cap=args.ref_decode_cap)
     rep.warm()
     Replay = _replay_backend_cls(stepspec)
-    end = tr["step_ends"][n_win - 1]
     prof = lambda n, r: BackendProfile(name=f"cpu-{n}", role=r, decode_s_per_token=1.0,  # noqa: E731
                                        prefill_tokens_per_s=1.0)
-    small = Replay(prof(names[0], BackendRole.SMALL), tr["small"], tr["window_start"][0], end[0], rep)
-    base = Replay(prof(names[1], BackendRole.BASE), tr["base"], tr["window_start"][1], end[1], rep)
     cfg = EngineConfig(threshold=AcceptanceThreshold(args.threshold), temperature=0.0,
                        token_budget=args.budget, max_step_tokens=args.max_step_tokens)
-    res = reng.run_trajectory(cfg, tr["problem"], small, base)
-    first = tr["fast_forward_steps"] + args.warmup
-    timed = [s for s in res.state.retained_steps if first <= s.index < first + args.steps]
-    assert len(timed) == args.steps, (len(timed), args.steps)
-    tokens = sum(s.token_count for s in timed)
-    # step cost = the CPU cost of the calls the engine made for it (the trace's
-    # per-step call boundaries); with a sampled replay the engine's own clock
-    # around score_step would see the sampled time, so it is not used
-    lo, hi = tr["step_ends"][args.warmup - 1], tr["step_ends"][n_win - 1]
-    secs = (sum(t for i, t in small.cost.items() if lo[0] <= i < hi[0])
-            + sum(t for i, t in base.cost.items() if lo[1] <= i < hi[1]))
+    tokens, secs, n_acc, cpu_s, first_idx = 0, 0.0, 0, 0.0, []
+    for w, nw, n in zip(wins, warm_w, per_w):
+        end = w["step_ends"][nw + n - 1]
+        small = Replay(prof(names[0], BackendRole.SMALL), w["small"], w["window_start"][0], end[0], rep)
+        base = Replay(prof(names[1], BackendRole.BASE), w["base"], w["window_start"][1], end[1], rep)
+        res = reng.run_trajectory(cfg, w["problem"], small, base)
+        first = w["fast_forward_steps"] + nw
+        timed = [st for st in res.state.retained_steps if first <= st.index < first + n]
+        assert len(timed) == n, (len(timed), n)
+        tokens += sum(st.token_count for st in timed)
+        n_acc += sum(1 for st in timed if st.producer.value == "Speculator")
+        # step cost = the CPU cost of the calls the engine made for it (the
+        # trace's per-step call boundaries); with a sampled replay the engine's
+        # own clock around score_step would see the sampled time, so it is not used
+        lo = w["step_ends"][nw - 1] if nw > 0 else w["window_start"]
+        secs += (sum(t for i, t in small.cost.items() if lo[0] <= i < end[0])
+                 + sum(t for i, t in base.cost.items() if lo[1] <= i < end[1]))
+        cpu_s += small.cpu_s + base.cpu_s
+        first_idx.append(first)
     value = round(tokens / secs, 3)
-    n_acc = sum(1 for s in timed if s.producer.value == "Speculator")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / args.steps, 1),
@@ -684,16 +746,16 @@ def run_reference(args) -> None:
         "config": bench_config(args, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": rep.threads, "kind": "port",
                          "sample": (f"reference stepspec engine ({ref_root}) over the recorded "
-                                    f"trajectory of task0000; its {args.warmup} warm-up + "
-                                    f"{args.steps} timed steps (indices {first - args.warmup}.."
-                                    f"{first + args.steps - 1}) execute every backend call at the "
+                                    f"trajectories of this benchmark's {P} windows (timed steps "
+                                    f"from indices {first_idx}, {args.warmup} warm-up steps before "
+                                    f"the first); every backend call of those steps executes at the "
                                     f"full {names[0]} / {names[1]} shapes on the host cores "
                                     f"(oracle/cpu_replay.py) on a bounded sample per call -- "
                                     f"{rep.sample_text()}; a step's latency = the CPU cost of "
                                     f"its calls")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "loop": {"tokens": tokens, "accepted_fraction": round(n_acc / args.steps, 3),
-                 "cpu_seconds_scaled": round(small.cpu_s + base.cpu_s, 1),
+                 "cpu_seconds_scaled": round(cpu_s, 1),
                  "cpu_seconds_spent": round(rep.wall_s, 1)},
         "wall_s": round(time.perf_counter() - t_start, 1),
     }), flush=True)
@@ -721,6 +783,9 @@ def main() -> None:
     ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="CPU work of the cpu_baseline sample (whole timed steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--windows", type=int, default=4,
+                    help="batch 1: the timed steps are split over this many problems' windows, "
+                         "each after its own fast-forward")
     ap.add_argument("--ref-layer-frac", type=float, default=0.125,
                     help="--impl reference: fraction of each model's layers run per call (scaled back)")
     ap.add_argument("--ref-decode-cap", type=int, default=16,

@@ -237,6 +237,9 @@ class EngineStats:
     def minus(self, other: "EngineStats") -> "EngineStats":
         return EngineStats(**{k: getattr(self, k) - getattr(other, k) for k in self.__dict__})
 
+    def plus(self, other: "EngineStats") -> "EngineStats":
+        return EngineStats(**{k: getattr(self, k) + getattr(other, k) for k in self.__dict__})
+
 
 @dataclass
 class _Pages:
