@@ -1264,7 +1264,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
           // in latency-bound phases longer than the shared-memory ring covers
           if (p.l2_ahead >= 0) {
             while (npf < nld + ahead) {
-              tma_prefetch_2d(pf.map, pf.col(), pf.row());
+              if (kTiled)  // one contiguous tile of the decode-layout weights
+                l2_prefetch(pf.tile(), (uint32_t)pf.bytes);
+              else
+                tma_prefetch_2d(pf.map, pf.col(), pf.row());
               pf.next(p, s_ph);
               ++npf;
             }
