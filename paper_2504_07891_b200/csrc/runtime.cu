@@ -291,14 +291,14 @@ struct Model {
     p.vec_prologue = 1;
     if (const char* v = getenv("SR_MK_VECPRO")) p.vec_prologue = atoi(v);
     // L2 prefetch run-ahead beyond the ring (tiles of the decode-layout copy).
-    // Measured (round 2, same box): 8 tiles speed up the chain-bound 1.5B by
+    // Measured (round 2, same box): 4-8 tiles speed up the chain-bound 1.5B by
     // 2 % (1.077 -> 1.056 ms/token at 2 K); any run-ahead slows the HBM-bound
     // 32B (10.89 -> 11.24 / 11.92 at 8 / 16 tiles).  On for models whose
     // layer streams < 256 MB (the draft), off otherwise.
     {
       const double layer_bytes = 2.0 * ((double)qkv_rows * d.d_model + (double)d.d_model * q_dim +
                                         3.0 * d.d_model * d.d_ffn);
-      p.l2_ahead = layer_bytes < 256e6 ? 8 : -1;
+      p.l2_ahead = layer_bytes < 256e6 ? 4 : -1;
     }
     if (const char* v = getenv("SR_MK_L2AHEAD")) p.l2_ahead = atoi(v);
     p.head_split = 0;  // SR_MK_HEADSPLIT=1: split a page's heads over idle CTAs (round 1; no gain with the tensor-core attention)
