@@ -675,7 +675,11 @@ class B200Backend(ModelBackend):
                  n_streams: int = 4, threshold: int = 7, max_new: int = 256,
                  max_tokens: int = 256, device: str = "cuda", init_device: str | None = None,
                  vocab: Vocab | None = None, types=None, record: bool = False,
-                 tp: "TensorParallel | None" = None) -> None:
+                 tp: "TensorParallel | None" = None, decode_layout: bool = True) -> None:
+        """``decode_layout``: keep the decode kernel's tile-major copy of the
+        streamed weights (``decode_tiles``; ~8 % faster decode for the 32B at
+        the cost of holding those weights twice); False streams the row-major
+        weights through TMA boxes with CUDA-core GEMVs."""
         if not torch.cuda.is_available():
             raise RuntimeError("B200Backend needs a CUDA device (no CPU fallback)")
         spec = get_spec(spec) if isinstance(spec, str) else spec
@@ -693,7 +697,8 @@ class B200Backend(ModelBackend):
         max_pos = max_ctx + max_new + 64
         pages_per_stream = math.ceil(max_pos / PAGE) + 1
         model = DeviceModel(spec, weights, max_pos=max_pos, n_pages=n_streams * pages_per_stream,
-                            max_tokens=max_tokens, max_new=max_new, device=device)
+                            max_tokens=max_tokens, max_new=max_new, device=device,
+                            decode_layout=decode_layout)
         if tp is not None and tp.comm is not None:
             native.check("sr_model_set_tp", model.lib.sr_model_set_tp(model.handle, tp.comm))
         if tp is not None and tp.peer is not None:

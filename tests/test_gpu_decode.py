@@ -187,3 +187,27 @@ def test_one_token_feed_decodes_on_the_oracle(cuda, name):
         text += r.text
     assert fed1 >= 3, fed1  # every continuation after the first call
     assert flagged <= max(2, checked // 20), (flagged, checked)  # near-ties are rare, not absent
+
+
+def test_row_major_decode_path_replays_on_oracle(cuda):
+    """``decode_layout=False``: no tile-major copy; the persistent kernel
+    streams the row-major weights through TMA boxes and runs its GEMVs on the
+    CUDA cores.  Its tokens replay on the oracle like the default path's."""
+    from paper_2504_07891_b200.backend import B200Backend
+    from paper_2504_07891_b200.contract import GenerationRequest
+
+    spec = get_spec("r1-1.5b")
+    w = make_weights(spec, 0)
+    v = shared_vocab(spec.vocab_text)
+    be = B200Backend(spec, BackendRole.SMALL, weights=w, max_ctx=1024, decode_layout=False)
+    assert not be.device_model.tiles
+    ref = RefEngine(spec, w, v)
+    tol = floor_tol("r1-1.5b")
+    prompt = render_generation_prompt(v.problem(64, 5), "")
+    r = be.generate_step(GenerationRequest(prompt=prompt, max_tokens=32, stop=()))
+    flagged = 0
+    for t, top, gap in _replay(ref, v.encode(prompt), v.encode(r.text), v.n_text):
+        if t != top:
+            assert gap < tol, (t, top, gap)
+            flagged += 1
+    assert flagged <= 2
