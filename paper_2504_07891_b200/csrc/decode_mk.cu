@@ -83,7 +83,7 @@ constexpr int kStageBytes = kUPS * kTileBytes;
 constexpr int kMkMaxStages = 13;
 constexpr int kMkMaxGq = 8;
 constexpr int kMkProfEvents = SR_PROF_EVENTS;
-constexpr int kMkAttnScratchFloats = 2048;  // attention q / P / row partials; COMBINE [16][32]+32
+constexpr int kMkAttnScratchFloats = 2048;  // attention q / P / row partials; COMBINE [16][64]+32
 constexpr int kMkTab = 256;  // max 32-row blocks of a tile-range phase (smem tables)
 constexpr int kKvBufBytes = 2 * kPage * kHeadDim * 2;  // K + V page (32 KB)
 
@@ -1057,70 +1057,100 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
 #undef SUB_EV
 }
 
-// COMBINE: merge the attention splits.  Work item = (query head, 32-dim slice),
-// spread over the grid; 16 thread groups each take every 16th split, one
-// round trip of loads, then a fixed-order merge of the groups (deterministic).
-SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, int hs, float* sm) {
+// COMBINE: merge the attention splits.  Work item = (query head, 32·NW-dim
+// slice), spread over the grid; 16 thread groups each take every 16th split,
+// one round trip of loads, then a fixed-order merge of the groups
+// (deterministic).  NW = 2 (64-dim items, float2 loads) when 32-dim items
+// would outnumber the CTAs (32B: 160 items on 148 CTAs, so 12 CTAs ran two
+// rounds and every CTA waited for them at the next barrier); the arithmetic
+// per (head, dim) is the same sequence either way, so the result is
+// bit-identical.
+template <int NW>
+SR_DEV void mk_combine_w(const MkParams& p, int c, int G, int S_a, int hs, float* sm) {
+  constexpr int W = 32 * NW, PER = kHeadDim / W, B = 4 / NW;  // B splits in flight
   const int Gq = p.H / p.KV;
   const int tid = threadIdx.x, dl = tid & 31, grp = tid >> 5;
-  float* r_o = sm;               // [16][32]
-  float* r_m = sm + 16 * 32;     // [16]
-  float* r_l = r_m + 16;         // [16]
-  for (int it = c; it < p.H * 4; it += G) {
-    const int h = it >> 2, d = (it & 3) * 32 + dl;
+  float* r_o = sm;                  // [16][W]
+  float* r_m = sm + kMkWarps * W;   // [16]
+  float* r_l = r_m + kMkWarps;      // [16]
+  for (int it = c; it < p.H * PER; it += G) {
+    const int h = it / PER, d = (it % PER) * W + dl * NW;
     const int g = h / Gq, j = h - g * Gq;
     // with head splits only the part owning head j holds data: splits s*hs + hp
     int hp = 0;
     while (hp + 1 < hs && Gq * (hp + 1) / hs <= j) ++hp;
-    float m = -INFINITY, l = 0.f, o = 0.f;
-    // this group's splits q0, q0 + qs, ...: four at a time, all loads issued
-    // before the (in-order, so unchanged) merge -- one L2 round trip per 4
-    const int q0 = grp * hs + hp, qs = kMkWarps * hs;
-    for (int qb = q0; qb < S_a; qb += 4 * qs) {
-      float ms[4], ls[4], os[4];
+    float m = -INFINITY, l = 0.f, o[NW];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+    for (int e = 0; e < NW; ++e) o[e] = 0.f;
+    // this group's splits q0, q0 + qs, ...: B at a time, all loads issued
+    // before the (in-order, so unchanged) merge -- one L2 round trip per B
+    const int q0 = grp * hs + hp, qs = kMkWarps * hs;
+    for (int qb = q0; qb < S_a; qb += B * qs) {
+      float ms[B], ls[B], os[B][NW];
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
         const int q = qb + i * qs;
         ms[i] = -INFINITY;
-        ls[i] = os[i] = 0.f;
+        ls[i] = 0.f;
+#pragma unroll
+        for (int e = 0; e < NW; ++e) os[i][e] = 0.f;
         if (q < S_a) {
           const float* a = p.apart + ((size_t)(g * S_a + q) * kMkMaxGq + j) * 130;
           ms[i] = __ldcg(a + 128);
           ls[i] = __ldcg(a + 129);
-          os[i] = __ldcg(a + d);
+          if constexpr (NW == 2) {
+            const float2 v = __ldcg(reinterpret_cast<const float2*>(a + d));  // 130·4 B rows: 8-B aligned
+            os[i][0] = v.x;
+            os[i][1] = v.y;
+          } else {
+            os[i][0] = __ldcg(a + d);
+          }
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < B; ++i) {
         if (ms[i] == -INFINITY) continue;  // past S_a, or a head-split slot of another head
         const float mn = fmaxf(m, ms[i]);
         const float x = exp2f(m - mn), y = exp2f(ms[i] - mn);
         l = l * x + ls[i] * y;
-        o = o * x + os[i] * y;
+#pragma unroll
+        for (int e = 0; e < NW; ++e) o[e] = o[e] * x + os[i][e] * y;
         m = mn;
       }
     }
-    r_o[grp * 32 + dl] = o;
+#pragma unroll
+    for (int e = 0; e < NW; ++e) r_o[grp * W + dl * NW + e] = o[e];
     if (dl == 0) {
       r_m[grp] = m;
       r_l[grp] = l;
     }
     cbar();
     if (grp == 0) {
-      float M = r_m[0], L = r_l[0], O = r_o[dl];
+      float M = r_m[0], L = r_l[0], O[NW];
+#pragma unroll
+      for (int e = 0; e < NW; ++e) O[e] = r_o[dl * NW + e];
       for (int q = 1; q < kMkWarps; ++q) {
         const float mq = r_m[q];
         if (mq == -INFINITY) continue;
         const float mn = fmaxf(M, mq);
         const float x = exp2f(M - mn), y = exp2f(mq - mn);
         L = L * x + r_l[q] * y;
-        O = O * x + r_o[q * 32 + dl] * y;
+#pragma unroll
+        for (int e = 0; e < NW; ++e) O[e] = O[e] * x + r_o[q * W + dl * NW + e] * y;
         M = mn;
       }
-      p.attn[(size_t)h * kHeadDim + d] = __float2bfloat16_rn(O / L);
+#pragma unroll
+      for (int e = 0; e < NW; ++e) p.attn[(size_t)h * kHeadDim + d + e] = __float2bfloat16_rn(O[e] / L);
     }
     cbar();
   }
+}
+
+SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, int hs, float* sm) {
+  if (p.combine_wide > 0 || (p.combine_wide < 0 && p.H * (kHeadDim / 32) > G))
+    mk_combine_w<2>(p, c, G, S_a, hs, sm);
+  else
+    mk_combine_w<1>(p, c, G, S_a, hs, sm);
 }
 
 // Walks this CTA's tile sequence: per token, layer 0..L-1 x (qkv, o, gate/up,

@@ -220,6 +220,7 @@ struct MkParams {
   int maxj, stages, xs_elems;
   int l2_ahead;              // tiles prefetched into L2 beyond the shared-memory ring
   int head_split;            // split a page's query heads over idle CTAs (short contexts)
+  int combine_wide;          // COMBINE items of 64 dims (1), 32 dims (0), or by item count (-1)
   int bar_sleep;             // ns of backoff between grid-barrier polls
   int evict_first;           // stream weights with an L2 evict-first policy
   int min_pages;             // attention: minimum K/V pages per split

@@ -303,6 +303,8 @@ struct Model {
     if (const char* v = getenv("SR_MK_L2AHEAD")) p.l2_ahead = atoi(v);
     p.head_split = 0;  // SR_MK_HEADSPLIT=1: split a page's heads over idle CTAs (round 1; no gain with the tensor-core attention)
     if (const char* v = getenv("SR_MK_HEADSPLIT")) p.head_split = atoi(v);
+    p.combine_wide = -1;  // SR_MK_COMBW=0/1: A/B of the 64-dim COMBINE items
+    if (const char* v = getenv("SR_MK_COMBW")) p.combine_wide = atoi(v);
     p.bar_sleep = 0;
     p.evict_first = 1;
     p.min_pages = 1;

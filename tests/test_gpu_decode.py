@@ -211,3 +211,30 @@ def test_row_major_decode_path_replays_on_oracle(cuda):
             assert gap < tol, (t, top, gap)
             flagged += 1
     assert flagged <= 2
+
+
+@pytest.mark.parametrize("name,ctx_len", [("tiny-base", 3000), ("r1-1.5b", 3000)])
+def test_combine_item_width_is_bit_identical(cuda, name, ctx_len):
+    """COMBINE merges the attention splits per (head, 32-dim) item, or per
+    (head, 64-dim) item with float2 loads when 32-dim items outnumber the CTAs
+    (the 32B).  Both run the same merge sequence per (head, dim), so forcing
+    either (SR_MK_COMBW=0/1) must give identical tokens and bit-identical
+    top-1/top-2 margins at a context with several splits per group."""
+    spec = get_spec(name)
+    w = make_weights(spec, 0)
+    v = shared_vocab(spec.vocab_text)
+    g = torch.Generator().manual_seed(11)
+    ctx = torch.randint(16, v.n_text, (ctx_len,), generator=g).tolist()
+    runs = []
+    for wide in ("0", "1"):
+        os.environ["SR_MK_COMBW"] = wide
+        try:
+            be = _backend(spec, w, max_ctx=ctx_len + 64)
+        finally:
+            os.environ.pop("SR_MK_COMBW", None)
+        gen, _ = be.engine.generate(be.pool.streams[0], ctx, 32, ())
+        runs.append((gen, list(be.engine.last_margins)))
+        del be
+        torch.cuda.empty_cache()
+    assert runs[0][0] == runs[1][0]
+    assert runs[0][1] == runs[1][1]
