@@ -1064,7 +1064,7 @@ SR_DEV void mk_attention(const MkParams& p, int layer, int pos, const int* page_
 // would outnumber the CTAs (32B: 160 items on 148 CTAs, so 12 CTAs ran two
 // rounds and every CTA waited for them at the next barrier); the arithmetic
 // per (head, dim) is the same sequence either way, so the result is
-// bit-identical.
+// bit-identical.  The width is a kernel template parameter (mk_launch).
 template <int NW>
 SR_DEV void mk_combine_w(const MkParams& p, int c, int G, int S_a, int hs, float* sm) {
   constexpr int W = 32 * NW, PER = kHeadDim / W, B = 4 / NW;  // B splits in flight
@@ -1146,13 +1146,6 @@ SR_DEV void mk_combine_w(const MkParams& p, int c, int G, int S_a, int hs, float
   }
 }
 
-SR_DEV void mk_combine(const MkParams& p, int c, int G, int S_a, int hs, float* sm) {
-  if (p.combine_wide > 0 || (p.combine_wide < 0 && p.H * (kHeadDim / 32) > G))
-    mk_combine_w<2>(p, c, G, S_a, hs, sm);
-  else
-    mk_combine_w<1>(p, c, G, S_a, hs, sm);
-}
-
 // Walks this CTA's tile sequence: per token, layer 0..L-1 x (qkv, o, gate/up,
 // down), then the LM head; wraps to the next token.  Empty phases are skipped.
 struct MkCursor {
@@ -1232,7 +1225,7 @@ SR_DEV void mk_prefetch_next_layer(const MkParams& p, int l, int pos, const int*
 // kTiled: the tile-major weights + mma.sync consumers (p.tiled), else row-major
 // TMA boxes + CUDA-core consumers; two instantiations, so each carries the
 // registers of one consumer only
-template <bool kTiled>
+template <bool kTiled, bool kWide>
 __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams p) {
   extern __shared__ __align__(1024) uint8_t mk_smem[];
   __shared__ __align__(8) uint64_t full[kMkMaxStages];
@@ -1433,7 +1426,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const MkParams
       MK_EV();  // 4 attention
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 5 sync
-      mk_combine(p, c, G, S_a, hs, scratch);
+      if constexpr (kWide) mk_combine_w<2>(p, c, G, S_a, hs, scratch); else mk_combine_w<1>(p, c, G, S_a, hs, scratch);
       MK_EV();  // 6 combine
       mk_grid_sync(bar, target, G, p.bar_sleep);
       MK_EV();  // 7 sync
@@ -1586,14 +1579,17 @@ int mk_tile_cols() { return kTC; }
 
 cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream) {
   const size_t smem = mk_smem_bytes(p.stages, p.xs_elems, p.kv_dbl);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(decode_mk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(decode_mk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // instantiations: consumer (tile-major mma.sync / row-major CUDA-core) x
+  // COMBINE item width, so each carries the registers of its own variants only
+  const bool wide = p.combine_wide > 0 || (p.combine_wide < 0 && p.H * (kHeadDim / 32) > num_sms);
+  auto* kern = p.tiled ? (wide ? decode_mk_kernel<true, true> : decode_mk_kernel<true, false>)
+                       : (wide ? decode_mk_kernel<false, true> : decode_mk_kernel<false, false>);
+  static size_t attr[4] = {0, 0, 0, 0};
+  size_t& a = attr[(p.tiled ? 2 : 0) + (wide ? 1 : 0)];
+  if (a < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    a = smem;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms);
@@ -1605,8 +1601,7 @@ cudaError_t mk_launch(const MkParams& p, int num_sms, cudaStream_t stream) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return p.tiled ? cudaLaunchKernelEx(&cfg, decode_mk_kernel<true>, p)
-                 : cudaLaunchKernelEx(&cfg, decode_mk_kernel<false>, p);
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 }  // namespace sr
