@@ -9,13 +9,14 @@ thinking budget, 64-word synthetic problems (``dp.problem_text``).  One
 public API (``driver.SpecReasonSession`` over two ``B200Backend``s): the draft
 decodes a step, the base scores it in one prefill pass, and on reject the base
 regenerates it.  The K timed steps are split over P = 4 windows
-(``--windows``), one per problem (task0000..), each mid-trajectory: an
-untimed fast-forward runs that problem's trajectory to a quarter of its
-thinking budget (2048 CoT tokens), then (first window only) W warm-up steps,
-then the window's share of the K timed steps, which at ~25-90 tokens per
-step cover contexts of ~2.5-6 K (an 8 K trajectory's mean is 4 K).  The loop
-metric follows the acceptance rate of the timed steps, so several problems'
-windows give a steadier number than one.
+(``--windows``), one per problem (task0000..), spread over the trajectory:
+an untimed fast-forward runs window i's trajectory to 0.75 * budget * (i +
+1/2) / P CoT tokens (768, 2304, 3840, 5376 of an 8 K budget: the acceptance
+rate drifts down along a trajectory, so windows that all started at one
+point over-weighted it), then (first window only) W warm-up steps, then the
+window's share of the K timed steps.  The loop metric follows the
+acceptance rate of the timed steps, so several problems' windows at several
+depths give a steadier number than one.
 
 Reported (one JSON line, rank 0):
   value      CoT tokens / s over the K timed steps, device time (sum of the
@@ -366,7 +367,7 @@ def run_ours(args) -> None:
             for i, n in enumerate(per_w):
                 wsrc = StepSource(small, base, cfg, [mine[i % len(mine)]], vocab)
                 start = (len(small.calls), len(base.calls))
-                ff_i = wsrc.fast_forward(ff)
+                ff_i = wsrc.fast_forward(window_ff(args, i, P))
                 c_ff = (len(small.calls), len(base.calls))
                 warm = []
                 for _ in range(args.warmup if i == 0 else 0):
@@ -512,6 +513,14 @@ def run_sweep(args) -> None:
         dist.destroy_process_group()
 
 
+def window_ff(args, i: int, P: int) -> int:
+    """CoT tokens window i of P fast-forwards to (batch 1): spread over the
+    first three quarters of the budget, or ``--ff-tokens`` for every window."""
+    if args.ff_tokens >= 0:
+        return args.ff_tokens
+    return int(0.75 * args.budget * (i + 0.5) / P)
+
+
 def bench_config(args, world: int) -> dict:
     """The ``config`` object both arms print (same_config)."""
     return {"workload": WORKLOADS[args.pair].replace("batch 1", f"batch {args.batch}"),
@@ -521,8 +530,8 @@ def bench_config(args, world: int) -> dict:
             "timed_window": (f"the timed steps split over {max(1, min(args.windows, args.steps))} "
                              f"windows on the first problems of the block, each after an untimed "
                              f"fast-forward to "
-                             f"{args.budget // 4 if args.ff_tokens < 0 else args.ff_tokens} CoT "
-                             f"tokens (warm-up steps before the first)"
+                             f"{[window_ff(args, i, max(1, min(args.windows, args.steps))) for i in range(max(1, min(args.windows, args.steps)))]} "
+                             f"CoT tokens (warm-up steps before the first)"
                              if args.batch == 1 else
                              f"after an untimed fast-forward of every trajectory to "
                              f"{args.budget // 4 if args.ff_tokens < 0 else args.ff_tokens} CoT "
@@ -778,7 +787,8 @@ def main() -> None:
     ap.add_argument("--problems", type=int, default=64,
                     help="fixed problem set task0000.. (split by id across DP ranks)")
     ap.add_argument("--ff-tokens", type=int, default=-1,
-                    help="untimed fast-forward to this many CoT tokens (-1: budget / 2)")
+                    help="untimed fast-forward to this many CoT tokens (-1: batch 1 spreads the "
+                         "windows over 0.75 * budget, --batch > 1 uses budget / 4)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="CPU work of the cpu_baseline sample (whole timed steps)")
