@@ -713,7 +713,10 @@ class B200Backend(ModelBackend):
                            decode_s_per_token=spec.decode_bytes(0) / 6.4e12,
                            prefill_tokens_per_s=1e4)
         self.device_model = model
-        super().__init__(NativeEngine(model, vocab), vocab, profile, n_streams=n_streams,
+        engine = NativeEngine(model, vocab)
+        if tp is not None:  # sr_score_batch / sr_step_batch are single-rank: no multi-span passes
+            engine.multi_span_passes = False
+        super().__init__(engine, vocab, profile, n_streams=n_streams,
                          threshold=threshold, types=types, record=record)
 
 

@@ -190,3 +190,23 @@ def test_tp2_peer_readout(tp2_results):
         lg = ref.model.forward(ref.model.new_cache(), a["ids"])
         want = judge_readout(lg, v, 7)
         assert a["score"] == want.score or readout_ambiguity(lg, v.n_text) < floor_tol("tiny-base")
+
+
+def test_tp1_loop_runs_and_validates(cuda):
+    """The whole loop with a tensor-parallel base (world size 1): a scoring
+    call after accepted drafts must not take the multi-span catch-up pass
+    (``sr_score_batch`` is single-rank), so the trajectory completes and
+    validates like the unsharded one (``bench.py --mode tp`` failed on its
+    first step before the guard)."""
+    from paper_2504_07891_b200 import AcceptanceThreshold, EngineConfig, run_trajectory
+    from paper_2504_07891_b200.backend import TensorParallel, build_pair
+    from paper_2504_07891_b200.driver import validate_trajectory
+
+    small, base = build_pair("tiny", max_ctx=2048, threshold=3, base_tp=TensorParallel.single())
+    assert base.engine.multi_span_passes is False
+    v = shared_vocab(get_spec("tiny-base").vocab_text)
+    cfg = EngineConfig(threshold=AcceptanceThreshold(3), temperature=0.0, token_budget=256,
+                       max_step_tokens=32)
+    res = run_trajectory(cfg, v.problem(64, 5), small, base)
+    validate_trajectory(res, cfg)
+    assert res.state.retained_steps
