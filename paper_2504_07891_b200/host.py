@@ -470,9 +470,14 @@ class ModelBackend(Backend):
         Only when at least two rows are missing: with one, the generation
         already starts in the decode kernel (``sr_generate``'s one-token path),
         which keeps a base that generates every step (threshold 10) computing
-        exactly what ``run_vanilla`` does."""
+        exactly what ``run_vanilla`` does.  Never on a trajectory's first step
+        (empty CoT): ``run_vanilla``'s first generation prefills the whole
+        prompt and takes its first token from that pass's LM head, so a
+        threshold-10 fallback must do the same rather than start in the
+        decode kernel."""
         if (not self.catch_up or self.verify_template != "v1" or len(self.pool.streams) < 2
-                or not getattr(self.engine, "multi_span_passes", False)):
+                or not getattr(self.engine, "multi_span_passes", False)
+                or not request.cot_prefix):
             return None
         gids = self._prompts.encode(domain.render_generation_prompt(request.problem,
                                                                     request.cot_prefix))
